@@ -1,0 +1,227 @@
+"""TEST INFRASTRUCTURE ONLY -- CPU oracle for the Shor hot path.
+
+Restates the reference ``shorsim`` algorithm (``/root/reference/pkg/src/shorsim``)
+for the stages the B200 path replaces, so the CUDA kernels can be checked
+on the same inputs.  Nothing in ``paper_1801_01434_b200`` imports this module;
+only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (the cpu_baseline
+leg and ``--impl reference``) do, and only as the checker / CPU baseline.
+
+Parity pin: ``tests/test_oracle_golden.py`` checks these functions against the
+golden vectors in ``tests/golden/`` that ``tests/golden/make_golden.py``
+produced by running the reference package itself.
+
+Heavy loops live in ``oracle/shor_oracle.c`` (built by ``oracle/Makefile``);
+this module holds the ctypes binding and the numpy-level restatements.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+_LIB_PATH = _HERE / "_build" / "liboracle.so"
+_lib = None
+
+
+def build() -> Path:
+    """Compile oracle/shor_oracle.c with the committed Makefile."""
+    subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
+    return _LIB_PATH
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            build()
+        L = ctypes.CDLL(str(_LIB_PATH))
+        u64, vp, i32, f64 = ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int, ctypes.c_double
+        L.oracle_roots.argtypes = [u64, u64, vp, vp]
+        L.oracle_dft_rows.argtypes = [u64, u64, vp, vp, u64, vp, i32, f64, vp, i32]
+        L.oracle_dense_rows_literal.argtypes = [u64, vp, u64, u64, u64, vp, vp, i32]
+        L.oracle_modexp.argtypes = [u64, u64, u64, u64, vp]
+        L.oracle_class_counts.argtypes = [vp, u64, u64, vp]
+        L.oracle_cumsum_search.argtypes = [vp, u64, f64, vp]
+        L.oracle_cumsum_search.restype = u64
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def default_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- twiddles
+
+def roots(q: int, idx) -> np.ndarray:
+    """Entries of qft.build_twiddles(q).roots at `idx` (qft.py:254), bitwise."""
+    idx = np.ascontiguousarray(idx, dtype=np.uint64)
+    out = np.empty(2 * idx.size, dtype=np.float64)
+    lib().oracle_roots(q, idx.size, _ptr(idx), _ptr(out))
+    return out.view(np.complex128)
+
+
+# ---------------------------------------------------------------- QFT rows
+
+def dft_rows(state_support, amps, q: int, rows, scale: bool = True,
+             threads: int | None = None) -> np.ndarray:
+    """Rows `rows` of qft.dense_dft (qft.py:270-287 / _kernels.py:16-30).
+
+    `state_support` are the ascending indices of the nonzero amplitudes and
+    `amps` their complex values.  With scale=True the 1/sqrt(q) factor is
+    applied exactly as qft.py:286 does; bitwise identical to the reference.
+    """
+    supp = np.ascontiguousarray(state_support, dtype=np.uint64)
+    a = np.ascontiguousarray(amps, dtype=np.complex128)
+    r = np.ascontiguousarray(rows, dtype=np.uint64)
+    if supp.size != a.size:
+        raise ValueError("support / amplitude length mismatch")
+    if supp.size > 1 and np.any(np.diff(supp.astype(np.int64)) <= 0):
+        raise ValueError("support must be strictly ascending")
+    out = np.empty(2 * r.size, dtype=np.float64)
+    s = 1.0 / math.sqrt(q)
+    lib().oracle_dft_rows(q, supp.size, _ptr(supp), _ptr(a.view(np.float64)),
+                          r.size, _ptr(r), 1 if scale else 0, s, _ptr(out),
+                          threads or default_threads())
+    return out.view(np.complex128)
+
+
+def dense_dft(state: np.ndarray, threads: int | None = None) -> np.ndarray:
+    """Whole reference dense_dft output for a dense state vector (any q)."""
+    state = np.ascontiguousarray(state, dtype=np.complex128)
+    q = state.size
+    nz = np.flatnonzero(state)
+    return dft_rows(nz, state[nz], q, np.arange(q, dtype=np.uint64), True, threads)
+
+
+def tiled_dft(state: np.ndarray, tiles: int, threads: int | None = None) -> np.ndarray:
+    """Reference tiled_dft (qft.py:290-317): per-segment partials, ascending add."""
+    state = np.ascontiguousarray(state, dtype=np.complex128)
+    q = state.size
+    seg = q // tiles
+    rows = np.arange(q, dtype=np.uint64)
+    out = None
+    for t in range(tiles):
+        lo, hi = t * seg, (t + 1) * seg
+        nz = np.flatnonzero(state[lo:hi]) + lo
+        part = dft_rows(nz, state[nz], q, rows, False, threads)
+        out = part.copy() if out is None else out + part
+    return out * (1.0 / math.sqrt(q))
+
+
+def dense_rows_literal(state: np.ndarray, rows, j0: int = 0, j1: int | None = None,
+                       threads: int | None = None) -> np.ndarray:
+    """_kernels.partial_row_sums over ALL j in [j0, j1) (zeros included), unscaled."""
+    state = np.ascontiguousarray(state, dtype=np.complex128)
+    q = state.size
+    j1 = q if j1 is None else j1
+    r = np.ascontiguousarray(rows, dtype=np.uint64)
+    out = np.empty(2 * r.size, dtype=np.float64)
+    lib().oracle_dense_rows_literal(q, _ptr(state.view(np.float64)), j0, j1, r.size,
+                                    _ptr(r), _ptr(out), threads or default_threads())
+    return out.view(np.complex128)
+
+
+# ---------------------------------------------------------------- modexp
+
+def modexp_residues(x: int, n: int, q: int, a_begin: int = 0) -> np.ndarray:
+    """entangle_modexp residues (qstate.py:94-113) as uint32, by recurrence."""
+    out = np.empty(q, dtype=np.uint32)
+    lib().oracle_modexp(x, n, a_begin, q, _ptr(out))
+    return out
+
+
+def modexp_residues_cycle(x: int, n: int, q: int) -> np.ndarray:
+    """The reference's own construction: one cycle of x^a, tiled to q (qstate.py:107-112)."""
+    seq = [1 % n]
+    v = x % n
+    while v != 1 % n:
+        seq.append(v)
+        v = v * x % n
+    return np.resize(np.asarray(seq, dtype=np.int64), q)
+
+
+# ---------------------------------------------------------------- collapse
+
+def class_counts(residues: np.ndarray, ncls: int) -> np.ndarray:
+    r = np.ascontiguousarray(residues, dtype=np.uint32)
+    out = np.empty(ncls, dtype=np.uint64)
+    lib().oracle_class_counts(_ptr(r), r.size, ncls, _ptr(out))
+    return out
+
+
+def measure_part2(amplitudes: np.ndarray, residues: np.ndarray, u: float):
+    """qstate.measure_part2 (qstate.py:116-135) on host arrays with draw u.
+
+    Returns (k, collapsed amplitude vector).
+    """
+    amps = np.asarray(amplitudes, dtype=np.complex128)
+    res = np.asarray(residues, dtype=np.int64)
+    w = np.abs(amps) ** 2
+    ncls = int(res.max()) + 1
+    probs = np.bincount(res, weights=w, minlength=ncls)
+    cdf = np.cumsum(probs)
+    k = min(int(np.searchsorted(cdf, u * cdf[-1], side="right")), ncls - 1)
+    sel = res == k
+    norm = np.sqrt(w[sel].sum())
+    out = np.zeros_like(amps)
+    out[sel] = amps[sel] / norm
+    return k, out
+
+
+# ---------------------------------------------------------------- sampling
+
+def probabilities(spectrum: np.ndarray) -> np.ndarray:
+    """|amp|**2 as qstate.py:141 computes it (np.abs -> hypot, then square)."""
+    return np.abs(np.asarray(spectrum, dtype=np.complex128)) ** 2
+
+
+def sample_index(probs: np.ndarray, u: float) -> int:
+    """qstate.sample_part1 tail (qstate.py:142-144) via the C sequential scan."""
+    p = np.ascontiguousarray(probs, dtype=np.float64)
+    return int(lib().oracle_cumsum_search(_ptr(p), p.size, u, None))
+
+
+def sample_index_numpy(probs: np.ndarray, u: float) -> int:
+    cdf = np.cumsum(probs)
+    m = int(np.searchsorted(cdf, u * cdf[-1], side="right"))
+    return min(m, probs.size - 1)
+
+
+# ---------------------------------------------------------------- closed form
+
+def comb_probabilities(q: int, r: int, c0: int, M: int, rows) -> np.ndarray:
+    """Independent closed form of |V_c|^2 for a uniform comb {c0 + j r}, j < M.
+
+    |V_c|^2 = sin^2(pi c r M / q) / (q M sin^2(pi c r / q)), and M/q when
+    c r = 0 mod q.  Phases are reduced exactly in integers to a signed residue
+    before the sine.  Not derived from the reference code;
+    used as a size-independent property check at q = 2^24..2^32.
+    """
+    rows = np.asarray(rows, dtype=np.uint64)
+    out = np.empty(rows.size, dtype=np.float64)
+    for i, c in enumerate(rows.tolist()):
+        a = (c * r) % q
+        if a == 0:
+            out[i] = M / q
+            continue
+        b = (c * r * M) % q
+        a_s = a - q if a > q // 2 else a
+        b_s = b - q if b > q // 2 else b
+        num = math.sin(math.pi * b_s / q)
+        den = math.sin(math.pi * a_s / q)
+        out[i] = (num * num) / (q * M * den * den)
+    return out

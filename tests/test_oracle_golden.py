@@ -1,0 +1,130 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself.
+
+These run without a GPU.  If any of them fails, the oracle is not a trustworthy
+checker and every GPU parity test downstream is meaningless.
+"""
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+
+
+@pytest.fixture(scope="module")
+def kats(golden_dir):
+    return json.loads((golden_dir / "kats.json").read_text())
+
+
+def _load_spec(golden_dir, tag):
+    d = np.load(golden_dir / f"spectrum_{tag}.npz")
+    return {k: d[k] for k in d.files}
+
+
+def test_root_table_bitwise(kats):
+    for q, vals in kats["twiddles"].items():
+        q = int(q)
+        got = oracle.roots(q, np.arange(q))
+        ref = np.array([complex(a, b) for a, b in vals])
+        assert np.array_equal(got.view(np.float64), ref.view(np.float64))
+    # wide tables: compare with numpy's own expression (qft.py:254) on samples
+    for w in (16, 24, 30, 32):
+        q = 1 << w
+        idx = np.random.default_rng(w).integers(0, q, 20000, dtype=np.uint64)
+        ref = np.exp((2j * np.pi / q) * idx.astype(np.int64))
+        assert np.array_equal(oracle.roots(q, idx).view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("tag", ["n15", "n15x2", "n221a1", "n221a2", "n3127"])
+def test_dft_rows_bitwise_vs_reference(golden_dir, tag):
+    d = _load_spec(golden_dir, tag)
+    info = json.loads(str(d["info"]))
+    q = int(d["q"])
+    M, c0, r = info["M"], info["c0"], info["r"]
+    amp = complex(np.uint64(int(info["amp_re_bits"], 16)).view(np.float64),
+                  np.uint64(int(info["amp_im_bits"], 16)).view(np.float64))
+    supp = c0 + r * np.arange(M, dtype=np.uint64)
+    amps = np.full(M, amp, dtype=np.complex128)
+    got = oracle.dft_rows(supp, amps, q, d["rows"])
+    # bitwise, signed zeros included
+    assert np.array_equal(got.view(np.uint64), d["V"].view(np.uint64))
+
+
+def test_literal_rows_match_support_rows(golden_dir):
+    d = _load_spec(golden_dir, "n221a2")
+    info = json.loads(str(d["info"]))
+    q = int(d["q"])
+    amp = np.uint64(int(info["amp_re_bits"], 16)).view(np.float64)
+    state = np.zeros(q, dtype=np.complex128)
+    state[info["c0"]::info["r"]] = amp
+    rows = d["rows"][:64]
+    lit = oracle.dense_rows_literal(state, rows) * (1.0 / math.sqrt(q))
+    assert np.array_equal(lit.view(np.uint64), d["V"][:64].view(np.uint64))
+
+
+def test_collapse_facts(golden_dir):
+    # n=15, x=2 forced k=1: support {0,4,...,252}, amplitude 1/8
+    d = _load_spec(golden_dir, "n15x2")
+    info = json.loads(str(d["info"]))
+    assert (info["k"], info["M"], info["c0"], info["r"]) == (1, 64, 0, 4)
+    p = np.abs(d["V"]) ** 2
+    # exact peak law
+    assert set(np.flatnonzero(p > 1e-20).tolist()) == {0, 64, 128, 192}
+    assert np.allclose(p[[0, 64, 128, 192]], 0.25, atol=1e-10)
+
+
+def test_random_states_dense_and_tiled(golden_dir):
+    d = np.load(golden_dir / "random_states.npz")
+    for key in ("16", "256", "1024", "4096", "sparse2048"):
+        z = d[f"{key}_state"]
+        ref_dense = d[f"{key}_dense"]
+        got = oracle.dense_dft(z)
+        assert np.array_equal(got.view(np.uint64), ref_dense.view(np.uint64)), key
+        got_t = oracle.tiled_dft(z, 8)
+        assert np.array_equal(got_t.view(np.uint64), d[f"{key}_tiled8"].view(np.uint64)), key
+
+
+def test_modexp_vs_reference_vectors(kats):
+    for q, x, n, res in kats["entangle"]:
+        assert oracle.modexp_residues(x, n, q).tolist() == res
+        assert oracle.modexp_residues_cycle(x, n, q).tolist() == res
+    # shard offsets agree with the full vector
+    full = oracle.modexp_residues(20637, 32399, 1 << 14)
+    assert np.array_equal(oracle.modexp_residues(20637, 32399, 4096, a_begin=8192), full[8192:12288])
+
+
+def test_measure_sweep_vs_reference(kats):
+    # k, support and amplitude bits for 1000+ draws including odd widths
+    seen = 0
+    for row in kats["measure_sweep"]:
+        q, x, n, u = row["q"], row["x"], row["n"], row["u"]
+        res = oracle.modexp_residues(x, n, q)
+        amps = np.full(q, 1.0 / math.sqrt(q), dtype=np.complex128)
+        k, out = oracle.measure_part2(amps, res, u)
+        assert k == row["k"]
+        supp = np.flatnonzero(out)
+        assert supp.size == row["M"] and supp[0] == row["c0"]
+        assert out[supp[0]].real.view(np.uint64) == np.uint64(int(row["amp_re_bits"], 16))
+        seen += 1
+    assert seen > 500
+
+
+def test_sampling_vs_reference(golden_dir):
+    d = np.load(golden_dir / "sampling.npz")
+    p = oracle.probabilities(d["state"])
+    for u, m in d["draws"]:
+        assert oracle.sample_index(p, float(u)) == int(m)
+        assert oracle.sample_index_numpy(p, float(u)) == int(m)
+
+
+def test_closed_form_comb_vs_reference_rows(golden_dir):
+    for tag in ("n221a1", "n221a2", "n3127"):
+        d = _load_spec(golden_dir, tag)
+        info = json.loads(str(d["info"]))
+        q = int(d["q"])
+        p_ref = np.abs(d["V"]) ** 2
+        p_cf = oracle.comb_probabilities(q, info["r"], info["c0"], info["M"], d["rows"])
+        # the reference dense rows themselves carry ~1e-11 accumulated rounding at 2^24
+        assert np.max(np.abs(p_cf - p_ref)) / np.max(p_ref) < 1e-10
