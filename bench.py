@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""QFT phase-terms/s and end-to-end factoring time at q = 2^30 (n = 32399) on B200.
+
+One step = one full Shor attempt on the device (modexp -> class counts ->
+collapse -> direct-DFT QFT -> exact Born-rule read), for n = 32399 = 179 x 181,
+q = 2^30, Sampler seed 8 (x = 10594, r = 16020, M = 67025 support elements:
+the attempt factors n through the quantum path).
+Phase terms per step = q * M (outputs x collapsed support).
+
+    python bench.py [--gpus N --steps K --warmup W] [--seed 2] [--impl reference]
+
+Under torchrun each rank owns q/N outputs and q/N exponents
+(paper_1801_01434_b200.distributed); total work is fixed -> strong scaling.
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "qft_phase_terms_per_s"
+UNIT = "phase_terms/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=2)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--n", type=int, default=32399)
+    p.add_argument("--seed", type=int, default=8)
+    p.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
+    p.add_argument("--max-width", type=int, default=32)
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--ref-step-seconds", type=float, default=6.0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-factoring", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+def workload(n: int, seed: int, max_width: int):
+    from paper_1801_01434_b200 import numtheory as nt
+    from paper_1801_01434_b200 import qstate, shor
+    rw = nt.choose_register_width(n, max_width)
+    s = qstate.Sampler(seed)
+    x = shor._draw_base(n, s)
+    if math.gcd(x, n) != 1:
+        raise SystemExit(f"seed {seed} draws x={x} sharing a factor with n={n}: pick another seed")
+    return rw.q, x
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def comb_of(n: int, x: int, q: int, seed: int):
+    """(k, c0, r, M, amp) of the attempt's collapsed register, on the host (exact ints)."""
+    from paper_1801_01434_b200 import numtheory as nt
+    from paper_1801_01434_b200 import qstate
+    r = nt.classical_period(x, n)
+    # class counts: residue x^a for a in [0, q) -> a mod r classes, count_j = floor((q-1-j)/r)+1
+    counts = {}
+    y = 1
+    for j in range(r):
+        counts[y] = (q - 1 - j) // r + 1
+        y = y * x % n
+    import numpy as np
+    carr = np.zeros(n, dtype=np.int64)
+    for v, c in counts.items():
+        carr[v] = c
+    s = qstate.Sampler(seed)
+    s.uniform()  # x draw
+    a_unif = complex(1.0 / math.sqrt(q))
+    w0 = qstate.uniform_weight(a_unif)
+    k = qstate.draw_class(carr, w0, s.uniform())
+    c0 = next(j for j in range(r) if pow(x, j, n) == k)
+    M = (q - 1 - c0) // r + 1
+    return k, c0, r, M, qstate.collapsed_amplitude(a_unif, w0, M)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7
+                          for i in range(4) if r[3 + i].lower() == "active"})
+        pw = [float(r[2]) for r in self.rows if len(r) >= 7 and r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm),
+                "power_w_max": max(pw) if pw else None}
+
+
+# ------------------------------------------------------------------ CPU legs
+
+def cpu_terms_rate(q: int, c0: int, r: int, M: int, amp: complex, seconds: float, threads: int):
+    """Oracle port of the reference dense engine (support-only rows, bit-identical
+    to _kernels.partial_row_sums) on a bounded sample of rows.  Test/baseline only."""
+    import numpy as np
+    from oracle import oracle
+    supp = c0 + r * np.arange(M, dtype=np.uint64)
+    amps = np.full(M, amp, dtype=np.complex128)
+    rng = np.random.default_rng(1)
+    rows_done = 0
+    batch = max(threads, 8)
+    t0 = time.perf_counter()
+    while True:
+        rows = rng.integers(0, q, batch, dtype=np.uint64)
+        oracle.dft_rows(supp, amps, q, rows, True, threads)
+        rows_done += batch
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+        batch = max(threads, int(batch * min(4.0, max(1.2, seconds / max(el, 1e-3) / 2))))
+    el = time.perf_counter() - t0
+    return rows_done * M / el, rows_done, el
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (oracle port) on the host cores."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    q, x = workload(args.n, args.seed, args.max_width)
+    k, c0, r, M, amp = comb_of(args.n, x, q, args.seed)
+    thr = cpu_threads()
+    for _ in range(args.warmup):
+        cpu_terms_rate(q, c0, r, M, amp, min(1.0, args.ref_step_seconds), thr)
+    rates, rows, secs = [], 0, 0.0
+    for _ in range(args.steps):
+        rate, nr, el = cpu_terms_rate(q, c0, r, M, amp, args.ref_step_seconds, thr)
+        rates.append(rate)
+        rows += nr
+        secs += el
+    value = rows * M / secs
+    sample = (f"{rows} random output rows of the n={args.n} q=2^{q.bit_length() - 1} attempt "
+              f"(M={M} support terms each) over {args.steps} steps of ~{args.ref_step_seconds:.0f}s")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (the collapsed register of the seeded attempt)",
+        "config": {"workload": f"n={args.n} q=2^{q.bit_length() - 1} seed={args.seed} x={x} M={M}",
+                   "n": args.n, "q": q, "x": x, "M": M, "precision": "fp64"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "port", "sample": sample,
+                         "cpu": cpu_model(),
+                         "note": "oracle/shor_oracle.c: support-only restatement of "
+                                 "_kernels.partial_row_sums, bit-identical output; the reference's "
+                                 f"own dense loop also walks the q-M zeros ({q / M:.0f}x more terms)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def run_b200(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1801_01434_b200 import _native as nat
+    from paper_1801_01434_b200 import build as buildmod
+    from paper_1801_01434_b200 import distributed as D
+    from paper_1801_01434_b200 import numtheory as nt
+    from paper_1801_01434_b200 import qstate, shor
+
+    if not nat.LIB_PATH.exists():
+        buildmod.build()
+    lib = nat.load()
+    q, x = workload(args.n, args.seed, args.max_width)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def one_step(time_dft=False):
+        s = qstate.Sampler(args.seed)
+        xx = shor._draw_base(args.n, s)
+        rec = D.sharded_attempt(args.n, xx, q, s, rank=rank, world=world, group=group,
+                                precision=args.precision, time_dft=time_dft)
+        est = nt.extract_period(rec.m, q, args.n, xx)
+        out = nt.derive_factors(args.n, xx, est.p) if isinstance(est, nt.PeriodCandidate) else est
+        return rec, out
+
+    for _ in range(args.warmup):
+        rec, outcome = one_step()
+    barrier()
+    uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+    clocks = ClockSampler(uuid)
+    clocks.start()
+    launches0 = lib.shb_kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record()
+    dft_ms, recs = [], []
+    for _ in range(args.steps):
+        rec, outcome = one_step(time_dft=True)
+        recs.append(rec)
+        dft_ms.append(rec.dft_ms)
+    e1.record()
+    barrier()
+    clk = clocks.stop()
+    launches = lib.shb_kernel_launches() - launches0
+    el_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([el_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        el_ms = float(t.item())
+    rec = recs[-1]
+    M = rec.M
+    terms_step = q * M
+    value = terms_step * args.steps / (el_ms / 1000.0)
+
+    # roofline of the dominant kernel (the DFT), per GPU
+    ptf = ctypes_double()
+    nat.check(lib.shb_fp64_peak(2.0, ptf, None), "fp64 peak")
+    peak_tf = ptf.value
+    dft_s = statistics.mean(dft_ms) / 1000.0
+    achieved_tf = 8.0 * rec.phase_terms / dft_s / 1e12
+    prof = ROOT / "profiles" / "dft_traffic.json"
+    traffic = None
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("bytes_per_launch_at_bench_config")
+        except Exception:
+            traffic = None
+    roof = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": achieved_tf / peak_tf, "traffic": traffic,
+            "peak_source": "measured on this GPU by shb_fp64_peak (independent DFMA chains); "
+                           "MEASURED_PEAKS.json has no FP64 figure; nominal 37.2 TF at 1965 MHz",
+            "kernel": "shb::dft_kernel<double>", "dft_ms_per_launch": dft_s * 1000.0,
+            "flops_per_launch": 8.0 * rec.phase_terms}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": el_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+        "data": "synthetic (the register is generated by the algorithm from n and the seed)",
+        "config": {"workload": f"n={args.n} (179x181) q=2^{q.bit_length() - 1} seed={args.seed} "
+                               f"x={x} r={rec.r} M={M}: one full attempt per step",
+                   "n": args.n, "q": q, "x": x, "k": rec.k, "r": rec.r, "M": M, "m": rec.m,
+                   "precision": args.precision, "parallelism": f"c/a-sharded x{world}",
+                   "l2": "no flush needed: each step writes 24 GiB (spectrum + |V|^2) >> 126 MB L2",
+                   "outcome": outcome.kind, "factors": list(outcome.factors) if outcome.factors else None},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "roofline": roof,
+        "phase_ms_last_step": {k: v * 1000 for k, v in rec.phase_times.items()},
+    }
+
+    # e2e: the reference-facing C-ABI drop-in with HOST buffers (dense_dft over a
+    # pinned complex128[q] state, H2D + DFT + D2H inside the timed region)
+    if not args.no_e2e and world == 1:
+        line["e2e"] = e2e_host(args, q, x, lib, torch, nat)
+    elif not args.no_e2e:
+        line["e2e"] = {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
+                       "path": "sharded pipeline from (n, seed); host-buffer e2e measured at N=1 only"}
+
+    if not args.no_factoring:
+        from paper_1801_01434_b200 import qft
+        barrier()
+        t0 = time.perf_counter()
+        if world == 1:
+            res = shor.run_shor(shor.ShorConfig(n=args.n, seed=args.seed, kernel="dense",
+                                                max_width=args.max_width,
+                                                plan=qft.KernelPlan(precision=args.precision)))
+            ft = time.perf_counter() - t0
+            line["factoring"] = {"api": "shor.run_shor", "time_s": ft, "factors": res.factors,
+                                 "attempts": len(res.attempts),
+                                 "ms": [a.m for a in res.attempts]}
+        else:
+            line["factoring"] = {"api": "distributed.sharded_attempt", "time_s": el_ms / args.steps / 1000,
+                                 "factors": list(outcome.factors) if outcome.factors else None}
+
+    if not args.no_cpu_baseline and world == 1 and rank == 0:
+        k, c0, r, Mh, amp = comb_of(args.n, x, q, args.seed)
+        thr = cpu_threads()
+        rate, rows, el = cpu_terms_rate(q, c0, r, Mh, amp, args.cpu_seconds, thr)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": thr, "kind": "port",
+                                "sample": f"{rows} random rows x M={Mh} terms of the same attempt in {el:.1f}s",
+                                "cpu": cpu_model()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def ctypes_double():
+    import ctypes
+    return ctypes.c_double(0.0)
+
+
+def e2e_host(args, q, x, lib, torch, nat):
+    import ctypes
+    import numpy as np
+    k, c0, r, M, amp = comb_of(args.n, x, q, args.seed)
+    st = torch.empty(2 * q, dtype=torch.float64, pin_memory=True)
+    out = torch.empty(2 * q, dtype=torch.float64, pin_memory=True)
+    stn = st.numpy().view(np.complex128)
+    stn[:] = 0
+    stn[c0::r] = amp
+    prec = 0 if args.precision == "fp64" else 1
+    steps = 1
+    # warm the path once at a small size (allocator pools, schedule upload)
+    small = np.zeros(1024, dtype=np.complex128)
+    small[3::7] = 0.1
+    so = np.empty_like(small)
+    nat.check(lib.shb_dense_dft_host(ctypes.c_void_p(small.ctypes.data), 1024, 1, prec,
+                                     ctypes.c_void_p(so.ctypes.data)))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        nat.check(lib.shb_dense_dft_host(ctypes.c_void_p(st.data_ptr()), q, 1, prec,
+                                         ctypes.c_void_p(out.data_ptr())), "dense_dft_host")
+    el = time.perf_counter() - t0
+    o = out.numpy().view(np.complex128)
+    peak = o[(q // r) * 0]
+    del st, out
+    return {"value": q * M * steps / el, "unit": UNIT, "h2d_bytes_per_step": 16 * q,
+            "d2h_bytes_per_step": 16 * q, "steps": steps, "seconds": el,
+            "api": "shb_dense_dft_host (C ABI of qft.dense_dft, pinned host buffers)",
+            "check_V0": [float(peak.real), float(peak.imag)]}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

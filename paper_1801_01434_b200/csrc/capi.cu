@@ -1,0 +1,302 @@
+// C ABI plumbing for libshorb200.so: error state, device info, scratch
+// allocation, the host-buffer drop-ins and the exact host-side helpers.
+#include <math.h>
+#include <float.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <map>
+
+#include "shb_internal.cuh"
+
+namespace shb {
+
+static thread_local char g_err[512] = "";
+static unsigned long long g_launches = 0;
+
+void note_launch(unsigned n) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
+
+int set_error(int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int check_cuda(cudaError_t e, const char *what)
+{
+    if (e == cudaSuccess) return SHB_OK;
+    const int code = (e == cudaErrorMemoryAllocation) ? SHB_ENOMEM : SHB_ECUDA;
+    cudaGetLastError();  // clear sticky-free errors so later calls can proceed
+    return set_error(code, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+int sm_count()
+{
+    static thread_local int cached_dev = -1, cached = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != cached_dev) {
+        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+        cached_dev = dev;
+    }
+    return cached > 0 ? cached : 148;
+}
+
+int scratch_alloc(Scratch &s, size_t bytes, cudaStream_t st)
+{
+    s.st = st;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(&s.ptr, bytes, st);
+    if (e != cudaSuccess) {
+        s.ptr = nullptr;
+        return check_cuda(e, "cudaMallocAsync(scratch)");
+    }
+    return SHB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Exact closed-form emulation of numpy reductions over a constant vector.
+
+// np.cumsum(np.full(n, w))[-1]: strict left-to-right float64 adds.  Within one
+// binade of the running sum S (ulp u) adding w moves S by a fixed number of
+// ulps d = round(w/u), so whole runs of adds are one multiply; the add that
+// leaves the binade is done in floating point.  Round-half-even ties only
+// depend on the parity of S/u, which is even after the first tied add.
+static double seqsum_const_impl(double w, uint64_t n)
+{
+    if (n == 0) return 0.0;
+    if (!(w > 0.0) || !isfinite(w)) {
+        double s = w;  // cumsum seeds with the first element
+        for (uint64_t i = 1; i < n; i++) s = s + w;
+        return s;
+    }
+    double S = w;
+    uint64_t done = 1;
+    const double two53 = 9007199254740992.0;
+    while (done < n) {
+        if (!isfinite(S)) {
+            return S;
+        }
+        double u, B;
+        if (S < ldexp(1.0, -1021)) {
+            u = ldexp(1.0, -1074);
+            B = ldexp(1.0, -1021);
+        } else {
+            int e;
+            frexp(S, &e);  // S in [2^(e-1), 2^e)
+            u = ldexp(1.0, e - 53);
+            B = ldexp(1.0, e);
+        }
+        const double Su = S / u;   // exact integer < 2^53
+        const double x = w / u;    // exact (w <= S)
+        const double kf = floor(x);
+        const double frac = x - kf;
+        double d;
+        if (frac < 0.5) {
+            d = kf;
+        } else if (frac > 0.5) {
+            d = kf + 1.0;
+        } else {
+            if (fmod(Su, 2.0) != 0.0) {  // odd: this one add decides by parity
+                S = S + w;
+                done++;
+                continue;
+            }
+            d = (fmod(kf, 2.0) == 0.0) ? kf : kf + 1.0;
+        }
+        if (d == 0.0) return S;  // every further add rounds back to S
+        // largest k with Su + k*d < 2^53 (stays strictly inside the binade)
+        const double room = two53 - Su;  // exact, > 0
+        double ksafe = ceil(room / d) - 1.0;
+        if (ksafe < 0) ksafe = 0;
+        const uint64_t rem = n - done;
+        const uint64_t take = (ksafe >= (double)rem) ? rem : (uint64_t)ksafe;
+        S = (Su + (double)take * d) * u;  // exact: integer < 2^53 times power of 2
+        done += take;
+        (void)B;
+        if (done < n) {  // the add that crosses into the next binade
+            S = S + w;
+            done++;
+        }
+    }
+    return S;
+}
+
+// numpy's pairwise summation (umath loops_utils pairwise_sum) specialised to
+// a constant input: blocks of <= 128 use 8 interleaved accumulators, larger
+// spans split at n/2 rounded down to a multiple of 8.  Memoised by length.
+struct PairwiseConst {
+    double w;
+    std::map<uint64_t, double> memo;
+    double run(uint64_t n)
+    {
+        auto it = memo.find(n);
+        if (it != memo.end()) return it->second;
+        double res;
+        if (n < 8) {
+            res = -0.0;
+            for (uint64_t i = 0; i < n; i++) res += w;
+        } else if (n <= 128) {
+            // r[k] = w + w + ... ((n - n%8)/8 copies, sequential)
+            const uint64_t per = (n - n % 8) / 8;
+            double r = seqsum_const_impl(w, per);
+            res = ((r + r) + (r + r)) + ((r + r) + (r + r));
+            for (uint64_t i = n - n % 8; i < n; i++) res += w;
+        } else {
+            uint64_t n2 = n / 2;
+            n2 -= n2 % 8;
+            res = run(n2) + run(n - n2);
+        }
+        memo[n] = res;
+        return res;
+    }
+};
+
+// FP64 FMA throughput probe: 8 independent DFMA chains per thread, a grid of
+// 4 CTAs x 256 threads per SM.  The roofline denominator of the QFT kernel.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double *out, int iters, double a, double b)
+{
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) x[i] = fma(x[i], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s += x[i];
+    if (s == 1234.5) out[0] = s;  // keep the chains alive
+}
+
+}  // namespace shb
+
+using namespace shb;
+
+extern "C" {
+
+int shb_abi_version(void) { return SHB_ABI_VERSION; }
+
+uint64_t shb_kernel_launches(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+const char *shb_last_error(void) { return g_err; }
+
+int shb_device_info(int device, int *sm, char *name, int name_len)
+{
+    cudaDeviceProp p;
+    SHB_TRY_CUDA(cudaGetDeviceProperties(&p, device));
+    if (sm) *sm = p.multiProcessorCount;
+    if (name && name_len > 0) {
+        strncpy(name, p.name, (size_t)name_len - 1);
+        name[name_len - 1] = 0;
+    }
+    return SHB_OK;
+}
+
+int shb_fp64_peak(double seconds, double *tflops, void *stream)
+{
+    if (!tflops) return set_error(SHB_EINVAL, "null output");
+    cudaStream_t st = as_stream(stream);
+    Scratch sink;
+    SHB_TRY(scratch_alloc(sink, sizeof(double), st));
+    const unsigned grid = (unsigned)sm_count() * 4;
+    const int iters = 1 << 16;
+    cudaEvent_t e0, e1;
+    SHB_TRY_CUDA(cudaEventCreate(&e0));
+    SHB_TRY_CUDA(cudaEventCreate(&e1));
+    fp64_probe_kernel<<<grid, 256, 0, st>>>((double *)sink.ptr, 1024, 0.999999, 1e-7);  // warm-up
+    SHB_LAUNCHED();
+    // size the timed loop to roughly `seconds`
+    int reps = 1;
+    float ms = 0.f;
+    for (;;) {
+        SHB_TRY_CUDA(cudaEventRecord(e0, st));
+        for (int r = 0; r < reps; r++) {
+            fp64_probe_kernel<<<grid, 256, 0, st>>>((double *)sink.ptr, iters, 0.999999, 1e-7);
+            SHB_LAUNCHED();
+        }
+        SHB_TRY_CUDA(cudaEventRecord(e1, st));
+        SHB_TRY_CUDA(cudaEventSynchronize(e1));
+        SHB_TRY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (ms >= seconds * 1000.0 * 0.5 || reps >= (1 << 16)) break;
+        reps *= 2;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * 8.0 * (double)iters * 256.0 * grid * reps;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    return SHB_OK;
+}
+
+double shb_host_seqsum_const(double w, uint64_t count) { return seqsum_const_impl(w, count); }
+
+double shb_host_pairwise_sum_const(double w, uint64_t count)
+{
+    PairwiseConst p{w, {}};
+    return p.run(count);
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer drop-ins: the C-level form of qft.dense_dft / tiled_dft and of
+// the _kernels.partial_row_sums seam.  Device memory is stream-ordered and
+// freed before return.
+
+static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t index_base,
+                           uint64_t q, uint64_t c_begin, uint64_t c_count, uint32_t tiles,
+                           double scale, int precision, double *out_host)
+{
+    cudaStream_t st = nullptr;
+    SHB_TRY_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } guard{st};
+    int rc = SHB_OK;
+    {
+        Scratch d_state, d_amps, d_out;
+        SHB_TRY(scratch_alloc(d_state, nstate * 16, st));
+        SHB_TRY_CUDA(cudaMemcpyAsync(d_state.ptr, state_host, nstate * 16, cudaMemcpyHostToDevice, st));
+        uint64_t a0 = 0, stride = 1, len = 0;
+        SHB_TRY(shb_state_progression((const double *)d_state.ptr, nstate, &a0, &stride, &len, st));
+        SHB_TRY(scratch_alloc(d_amps, (len ? len : 1) * 16, st));
+        if (len) SHB_TRY(shb_gather_progression((const double *)d_state.ptr, a0, stride, len,
+                                                (double *)d_amps.ptr, st));
+        SHB_TRY(scratch_alloc(d_out, c_count * 16, st));
+        rc = shb_dft((const double *)d_amps.ptr, len, a0 + index_base, stride, q, c_begin, c_count,
+                     tiles, scale, precision, (double *)d_out.ptr, nullptr, nullptr, st);
+        if (rc != SHB_OK) return rc;
+        SHB_TRY_CUDA(cudaMemcpyAsync(out_host, d_out.ptr, c_count * 16, cudaMemcpyDeviceToHost, st));
+    }
+    SHB_TRY_CUDA(cudaStreamSynchronize(st));
+    return rc;
+}
+
+int shb_dense_dft_host(const double *state, uint64_t q, uint32_t tiles, int precision, double *out)
+{
+    if (!state || !out) return set_error(SHB_EINVAL, "null buffer");
+    if (q < 2 || (q & (q - 1))) return set_error(SHB_EINVAL, "q must be a power of two >= 2, got %llu",
+                                                 (unsigned long long)q);
+    if (tiles < 1 || q % tiles) return set_error(SHB_EINVAL, "tiles %u does not divide q", tiles);
+    return dft_host_common(state, q, 0, q, 0, q, tiles, 1.0 / sqrt((double)q), precision, out);
+}
+
+int shb_partial_row_sums_host(double *out, const double *state, const double *roots, uint64_t q,
+                              uint64_t k0, uint64_t k1, uint64_t j0, uint64_t j1)
+{
+    (void)roots;
+    if (!state || !out) return set_error(SHB_EINVAL, "null buffer");
+    if (q < 2 || (q & (q - 1))) return set_error(SHB_EINVAL, "q must be a power of two >= 2");
+    if (k1 < k0 || k1 > q || j1 < j0 || j1 > q) return set_error(SHB_EINVAL, "row/column range outside [0, q)");
+    if (k1 == k0) return SHB_OK;
+    if (j1 == j0) {
+        memset(out, 0, (k1 - k0) * 16);
+        return SHB_OK;
+    }
+    return dft_host_common(state + 2 * j0, j1 - j0, j0, q, k0, k1 - k0, 1, 1.0, SHB_FP64, out);
+}
+
+}  // extern "C"

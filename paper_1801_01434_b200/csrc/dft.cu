@@ -1,0 +1,299 @@
+// Stage 3 of the hot path: the QFT as a direct DFT over the collapsed support
+// (qft.dense_dft / qft.tiled_dft, qft.py:270-317; inner loop
+// _kernels.partial_row_sums, _kernels.py:16-30).
+//
+//   V_c = scale * sum_j amp_j * e^{+2 pi i (a0 + j*stride) c / q}
+//
+// Only the support progression a_j = a0 + j*stride is visited, so one
+// transform is q*M phase terms (the reference also walks the q-M zeros).
+//
+// Per output c the phase advances by a constant rotation between successive
+// support elements, w_c = e^{-2 pi i stride c / q} (exact integer index ->
+// sincospi), so a segment of the sum is a polynomial in w_c evaluated by
+// Horner's rule in ascending j:
+//
+//   acc <- acc * w_c + amp_j          (4 DFMA = the 8 flops of one phase term)
+//   segment value = e^{2 pi i a_last c / q} * acc   (exact sincospi re-seed)
+//
+// Segments are re-seeded every SEG terms (rounding growth <= SEG*eps) and
+// tile partials (reference tiles, qft.py:306-316) are added in ascending
+// tile order.  Each thread owns K outputs (K independent FMA chains); the
+// amplitude stream is shared by the whole CTA and staged into shared memory
+// by TMA bulk copies (cp.async.bulk + mbarrier, multi-stage ring), so the
+// inner loop is LDS.128 broadcast + 4K DFMA: FP64-pipe bound.
+//
+// The epilogue fuses |V|^2 (hypot^2, as np.abs(.)**2, qstate.py:141) and a
+// deterministic per-CTA sum of it (norm check, qstate.py:50-53).
+#include <math.h>
+#include <vector>
+
+#include "shb_internal.cuh"
+
+namespace shb {
+
+enum : uint32_t { CH_SEG_END = 1u, CH_TILE_END = 2u };
+
+struct ChunkDesc {
+    uint64_t j0;
+    uint32_t cnt;
+    uint32_t flags;
+};
+
+constexpr int DFT_THREADS = 256;
+constexpr int DFT_STAGES = 4;
+constexpr int DFT_CHUNK = 1024;  // amplitudes per stage (16 KB)
+
+template <typename R>
+struct Prec;
+template <>
+struct Prec<double> {
+    static constexpr int K = 4;            // outputs per thread
+    static constexpr uint64_t SEG = 8192;  // terms between exact re-seeds
+};
+template <>
+struct Prec<float> {
+    static constexpr int K = 4;
+    static constexpr uint64_t SEG = 256;
+};
+
+// e^{+2 pi i idx / q} for an exact integer phase index (idx < q); the index
+// is folded to (-q/2, q/2] so sincospi's argument is in (-1, 1] and exact.
+__device__ __forceinline__ void phase(uint64_t idx, uint64_t q, double two_over_q, double &c, double &s)
+{
+    const int64_t sidx = (idx > (q >> 1)) ? (int64_t)(idx - q) : (int64_t)idx;
+    sincospi((double)sidx * two_over_q, &s, &c);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(DFT_THREADS, 2)
+    dft_kernel(const double2 *__restrict__ amps, const ChunkDesc *__restrict__ sched, uint32_t nchunks,
+               uint64_t a0, uint64_t stride, uint64_t q, double two_over_q, uint64_t c_begin,
+               uint64_t c_count, double scale, double2 *__restrict__ out, double *__restrict__ prob,
+               double *__restrict__ block_sums)
+{
+    constexpr int K = Prec<R>::K;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double2 *buf = reinterpret_cast<double2 *>(smem_raw);
+    __shared__ __align__(8) uint64_t full_bar[DFT_STAGES];
+    __shared__ double red_tmp[DFT_THREADS / 32];
+
+    const int tid = threadIdx.x;
+    const uint64_t qmask = q - 1;
+    const uint64_t cblk = (uint64_t)blockIdx.x * DFT_THREADS * K;
+
+    // per-output state: step rotation w (conj of e^{i phi}), Horner acc,
+    // tile partial t, running total v.
+    R wr[K], wi[K], hr[K], hi[K];
+    double tr[K], ti[K], vr[K], vi[K];
+    uint64_t cval[K];
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+        const uint64_t ci = cblk + (uint64_t)i * DFT_THREADS + tid;  // offset inside [0, c_count)
+        cval[i] = c_begin + ci;
+        double co, si;
+        phase((stride * cval[i]) & qmask, q, two_over_q, co, si);
+        wr[i] = (R)co;
+        wi[i] = (R)si;  // acc * (co - i si) is done below with +/- signs
+        hr[i] = hi[i] = (R)0;
+        tr[i] = ti[i] = vr[i] = vi[i] = 0.0;
+    }
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < DFT_STAGES; s++) mbar_init(&full_bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    auto issue = [&](uint32_t ch) {
+        const ChunkDesc d = sched[ch];
+        const int s = ch % DFT_STAGES;
+        const uint32_t bytes = d.cnt * 16u;
+        mbar_arrive_expect_tx(&full_bar[s], bytes);
+        tma_bulk_g2s(buf + (size_t)s * DFT_CHUNK, amps + d.j0, bytes, &full_bar[s]);
+    };
+    if (tid == 0) {
+        const uint32_t pro = nchunks < DFT_STAGES ? nchunks : DFT_STAGES;
+        for (uint32_t ch = 0; ch < pro; ch++) issue(ch);
+    }
+
+    for (uint32_t ch = 0; ch < nchunks; ch++) {
+        const int s = ch % DFT_STAGES;
+        const ChunkDesc d = sched[ch];
+        mbar_wait(&full_bar[s], (ch / DFT_STAGES) & 1u);
+        const double2 *sb = buf + (size_t)s * DFT_CHUNK;
+        const int cnt = (int)d.cnt;
+        int e = 0;
+        for (; e + 4 <= cnt; e += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const double2 av = sb[e + u];
+                const R a_re = (R)av.x, a_im = (R)av.y;
+#pragma unroll
+                for (int i = 0; i < K; i++) {
+                    // acc * conj(e^{i phi}) + a:
+                    //   re = acc_re cos + acc_im sin + a_re
+                    //   im = acc_im cos - acc_re sin + a_im
+                    const R t_re = fma(hi[i], wi[i], a_re);
+                    const R t_im = fma(hi[i], wr[i], a_im);
+                    const R n_re = fma(hr[i], wr[i], t_re);
+                    const R n_im = fma(-hr[i], wi[i], t_im);
+                    hr[i] = n_re;
+                    hi[i] = n_im;
+                }
+            }
+        }
+        for (; e < cnt; e++) {
+            const double2 av = sb[e];
+            const R a_re = (R)av.x, a_im = (R)av.y;
+#pragma unroll
+            for (int i = 0; i < K; i++) {
+                const R t_re = fma(hi[i], wi[i], a_re);
+                const R t_im = fma(hi[i], wr[i], a_im);
+                const R n_re = fma(hr[i], wr[i], t_re);
+                const R n_im = fma(-hr[i], wi[i], t_im);
+                hr[i] = n_re;
+                hi[i] = n_im;
+            }
+        }
+        if (d.flags & CH_SEG_END) {
+            // seed = e^{+2 pi i a_last c / q}; t += seed * acc; acc = 0
+            const uint64_t a_last = a0 + (d.j0 + d.cnt - 1) * stride;
+#pragma unroll
+            for (int i = 0; i < K; i++) {
+                double sc, ss;
+                phase((a_last * cval[i]) & qmask, q, two_over_q, sc, ss);
+                const double xr = (double)hr[i], xi = (double)hi[i];
+                tr[i] = fma(sc, xr, fma(-ss, xi, tr[i]));
+                ti[i] = fma(sc, xi, fma(ss, xr, ti[i]));
+                hr[i] = hi[i] = (R)0;
+            }
+        }
+        if (d.flags & CH_TILE_END) {
+#pragma unroll
+            for (int i = 0; i < K; i++) {
+                vr[i] += tr[i];
+                vi[i] += ti[i];
+                tr[i] = ti[i] = 0.0;
+            }
+        }
+        __syncthreads();  // every warp is done with stage s
+        if (tid == 0 && ch + DFT_STAGES < nchunks) issue(ch + DFT_STAGES);
+    }
+
+    // epilogue: scale (out *= 1/sqrt(q), qft.py:286), |V|^2, block sum
+    double psum = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+        const uint64_t ci = cblk + (uint64_t)i * DFT_THREADS + tid;
+        if (ci < c_count) {
+            const double o_re = vr[i] * scale, o_im = vi[i] * scale;
+            out[ci] = make_double2(o_re, o_im);
+            const double h = hypot(o_re, o_im);
+            const double p = h * h;
+            if (prob) prob[ci] = p;
+            psum += p;
+        }
+    }
+    if (block_sums) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) psum += __shfl_down_sync(0xffffffffu, psum, o);
+        if ((tid & 31) == 0) red_tmp[tid >> 5] = psum;
+        __syncthreads();
+        if (tid == 0) {
+            double b = 0.0;
+#pragma unroll
+            for (int w = 0; w < DFT_THREADS / 32; w++) b += red_tmp[w];
+            block_sums[blockIdx.x] = b;
+        }
+    }
+}
+
+template <typename R>
+static int launch_dft(const double *d_amps, uint64_t length, uint64_t a0, uint64_t stride, uint64_t q,
+                      uint64_t c_begin, uint64_t c_count, uint32_t tiles, double scale, double *d_out,
+                      double *d_prob, double *d_block_sums, cudaStream_t st)
+{
+    constexpr int K = Prec<R>::K;
+    const uint64_t SEG = Prec<R>::SEG;
+    // ---- chunk schedule: tiles -> re-seed segments -> smem chunks
+    std::vector<ChunkDesc> sched;
+    sched.reserve(length / DFT_CHUNK + tiles + length / SEG + 4);
+    const uint64_t tile_span = q / tiles;
+    for (uint32_t t = 0; t < tiles && length; t++) {
+        const uint64_t lo_a = (uint64_t)t * tile_span, hi_a = lo_a + tile_span;
+        auto first_j_at_or_above = [&](uint64_t a) -> uint64_t {
+            if (a <= a0) return 0;
+            const uint64_t j = (a - a0 + stride - 1) / stride;
+            return j < length ? j : length;
+        };
+        const uint64_t jlo = first_j_at_or_above(lo_a), jhi = first_j_at_or_above(hi_a);
+        if (jhi <= jlo) continue;
+        for (uint64_t s0 = jlo; s0 < jhi; s0 += SEG) {
+            const uint64_t s1 = (s0 + SEG < jhi) ? s0 + SEG : jhi;
+            for (uint64_t c0 = s0; c0 < s1; c0 += DFT_CHUNK) {
+                const uint64_t c1 = (c0 + DFT_CHUNK < s1) ? c0 + DFT_CHUNK : s1;
+                ChunkDesc d{c0, (uint32_t)(c1 - c0), 0u};
+                if (c1 == s1) d.flags |= CH_SEG_END;
+                if (c1 == s1 && s1 == jhi) d.flags |= CH_TILE_END;
+                sched.push_back(d);
+            }
+        }
+    }
+    const uint32_t nchunks = (uint32_t)sched.size();
+    Scratch d_sched;
+    SHB_TRY(scratch_alloc(d_sched, sizeof(ChunkDesc) * (nchunks ? nchunks : 1), st));
+    if (nchunks)
+        SHB_TRY_CUDA(cudaMemcpyAsync(d_sched.ptr, sched.data(), sizeof(ChunkDesc) * nchunks,
+                                     cudaMemcpyHostToDevice, st));
+    const size_t smem = (size_t)DFT_STAGES * DFT_CHUNK * sizeof(double2);
+    static bool attr_done = false;
+    if (!attr_done) {
+        SHB_TRY_CUDA(cudaFuncSetAttribute(dft_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_done = true;
+    }
+    const uint64_t per_blk = (uint64_t)DFT_THREADS * K;
+    const uint64_t nblk = (c_count + per_blk - 1) / per_blk;
+    if (nblk > 0x7FFFFFFFull) return set_error(SHB_EINVAL, "too many outputs for one launch");
+    dft_kernel<R><<<(unsigned)nblk, DFT_THREADS, smem, st>>>(
+        (const double2 *)d_amps, (const ChunkDesc *)d_sched.ptr, nchunks, a0, stride, q, 2.0 / (double)q,
+        c_begin, c_count, scale, (double2 *)d_out, d_prob, d_block_sums);
+    SHB_LAUNCHED();
+    SHB_TRY_CUDA(cudaGetLastError());
+    return SHB_OK;
+}
+
+}  // namespace shb
+
+using namespace shb;
+
+extern "C" uint64_t shb_dft_num_blocks(uint64_t c_count, int precision)
+{
+    const int K = (precision == SHB_FP32) ? Prec<float>::K : Prec<double>::K;
+    const uint64_t per = (uint64_t)DFT_THREADS * K;
+    return (c_count + per - 1) / per;
+}
+
+extern "C" int shb_dft(const double *d_amps, uint64_t length, uint64_t a0, uint64_t stride, uint64_t q,
+                       uint64_t c_begin, uint64_t c_count, uint32_t tiles, double scale, int precision,
+                       double *d_out, double *d_prob, double *d_block_sums, void *stream)
+{
+    if (q < 2 || (q & (q - 1))) return set_error(SHB_EINVAL, "q must be a power of two >= 2");
+    if (tiles < 1 || q % tiles) return set_error(SHB_EINVAL, "tiles %u does not divide q", tiles);
+    if (stride == 0) return set_error(SHB_EINVAL, "stride must be >= 1");
+    if (c_begin > q || c_count > q - c_begin) return set_error(SHB_EINVAL, "output rows outside [0, q)");
+    if (length && (a0 >= q || (length - 1) > (q - 1 - a0) / stride))
+        return set_error(SHB_EINVAL, "support progression leaves [0, q)");
+    if (precision != SHB_FP64 && precision != SHB_FP32) return set_error(SHB_EINVAL, "unknown precision %d", precision);
+    if (c_count == 0) return SHB_OK;
+    if (!d_out) return set_error(SHB_EINVAL, "null output buffer");
+    if (length && !d_amps) return set_error(SHB_EINVAL, "null amplitude buffer");
+    if (length && (reinterpret_cast<uintptr_t>(d_amps) & 15))
+        return set_error(SHB_EINVAL, "amplitude buffer must be 16-byte aligned");
+    cudaStream_t st = as_stream(stream);
+    if (precision == SHB_FP32)
+        return launch_dft<float>(d_amps, length, a0, stride, q, c_begin, c_count, tiles, scale, d_out, d_prob,
+                                 d_block_sums, st);
+    return launch_dft<double>(d_amps, length, a0, stride, q, c_begin, c_count, tiles, scale, d_out, d_prob,
+                              d_block_sums, st);
+}

@@ -1,0 +1,424 @@
+// Stage 4 (tail of the hot path): Born-rule read of part 1
+// (qstate.sample_part1 / l2_norm, qstate.py:138-148).
+//
+//   probs = np.abs(amp)**2 ; cum = np.cumsum(probs)
+//   m = searchsorted(cum, u*cum[-1], side="right")
+//
+// np.cumsum is a strictly sequential chain of float64 adds, and a parallel
+// scan rounds differently, which flips m near CDF boundaries.  This file
+// reproduces the sequential chain EXACTLY on the GPU.  While the running sum
+// S stays inside one binade [2^e, 2^(e+1)) with ulp u, the float add
+// fl(S + p) equals S + u*round(p/u) (ties: round-half-even on the parity of
+// S/u + floor(p/u)).  So inside a binade the chain is an exact INTEGER prefix
+// sum of per-element increments, which a CTA computes with a block scan; the
+// one add that leaves the binade is done in floating point, and rare ties are
+// resolved in order by one thread.  The result is bit-identical to numpy for
+// any input (tests/test_gpu_parity.py checks adversarial vectors).
+//
+// Pass 1 (one CTA, sequential over 8192-element chunks) yields cum[-1] and
+// the exact running sum at every chunk start; pass 2 re-walks only the one
+// chunk that contains u*cum[-1].
+#include <math.h>
+
+#include <vector>
+
+#include "shb_internal.cuh"
+
+namespace shb {
+
+// ------------------------------------------------------------ probabilities
+__global__ void prob_kernel(const double2 *__restrict__ v, uint64_t n, double *__restrict__ p)
+{
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += step) {
+        const double2 z = v[i];
+        const double h = hypot(z.x, z.y);
+        p[i] = h * h;
+    }
+}
+
+// ------------------------------------------------- deterministic tree sum
+constexpr int SUM_THREADS = 512;
+constexpr int SUM_BLOCKS = 1024;
+
+__device__ inline double block_sum(double v, double *tmp)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) tmp[wid] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) r += tmp[w];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(SUM_THREADS) sum_partial_kernel(const double *__restrict__ x, uint64_t n,
+                                                                  double *__restrict__ part)
+{
+    __shared__ double tmp[SUM_THREADS / 32];
+    // fixed assignment: block b owns a contiguous slice -> order independent of the GPU
+    const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = per * blockIdx.x, hi = (lo + per < n) ? lo + per : n;
+    double s = 0.0;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += SUM_THREADS) s += x[i];
+    const double b = block_sum(s, tmp);
+    if (threadIdx.x == 0) part[blockIdx.x] = b;
+}
+
+__global__ void __launch_bounds__(SUM_THREADS) sum_final_kernel(const double *__restrict__ part, int n,
+                                                                double *__restrict__ out)
+{
+    __shared__ double tmp[SUM_THREADS / 32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += SUM_THREADS) s += part[i];
+    const double b = block_sum(s, tmp);
+    if (threadIdx.x == 0) *out = b;
+}
+
+// --------------------------------------------- exact sequential cumsum walk
+constexpr int SEQ_THREADS = 1024;
+constexpr int SEQ_V = 8;                           // elements per thread per chunk
+constexpr int SEQ_CHUNK = SEQ_THREADS * SEQ_V;     // 8192
+constexpr uint64_t SAT = 1ull << 62;               // saturation for the unit scan
+constexpr uint64_t TWO53 = 1ull << 53;
+
+__device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b)
+{
+    const uint64_t s = a + b;
+    return s > SAT ? SAT : s;
+}
+
+// ulp of S and the power of two where it next changes
+__device__ __forceinline__ void binade(double S, double &u, double &B)
+{
+    if (S < 0x1p-1021) {
+        u = 0x1p-1074;
+        B = 0x1p-1021;
+    } else {
+        int e;
+        frexp(S, &e);  // S in [2^(e-1), 2^e)
+        u = ldexp(1.0, e - 53);
+        B = ldexp(1.0, e);
+    }
+}
+
+struct SeqShared {
+    uint64_t warp_tmp[SEQ_THREADS / 32];
+    uint32_t warp_min[SEQ_THREADS / 32];
+    uint64_t P[SEQ_CHUNK];        // inclusive unit prefix of the current range
+    uint64_t add[SEQ_CHUNK];      // per-element unit increments
+    uint8_t tie[SEQ_CHUNK];
+    double S;                     // exact running sum before `start`
+    int start;                    // first unprocessed local index
+    int done;
+    uint64_t found;
+};
+
+// block-wide saturating inclusive scan over thread totals -> exclusive offset
+__device__ inline uint64_t block_excl_sat(uint64_t v, uint64_t *warp_tmp)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = sat_add(x, y);
+    }
+    if (lane == 31) warp_tmp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint64_t w = warp_tmp[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w = sat_add(w, y);
+        }
+        warp_tmp[lane] = w;
+    }
+    __syncthreads();
+    const uint64_t before_warp = wid ? warp_tmp[wid - 1] : 0;
+    // x - v is exact unless saturated; recompute exclusive as sat(before_warp + (x excl v))
+    uint64_t excl_in_warp = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) excl_in_warp = 0;
+    __syncthreads();
+    return sat_add(before_warp, excl_in_warp);
+}
+
+__device__ inline int block_min_int(int v, uint32_t *warp_min)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_down_sync(0xffffffffu, v, o));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) warp_min[wid] = (uint32_t)v;
+    __syncthreads();
+    int r = (int)warp_min[0];
+    for (int w = 1; w < SEQ_THREADS / 32; w++) r = min(r, (int)warp_min[w]);
+    __syncthreads();
+    return r;
+}
+
+// Walk chunks [chunk_lo, chunk_hi) of p starting from the exact running sum
+// S0.  mode 0: record S at every chunk start (chunk_S) and the total.
+// mode 1: find the first index whose running sum exceeds `target`.
+__global__ void __launch_bounds__(SEQ_THREADS, 1)
+    seqscan_kernel(const double *__restrict__ p, uint64_t L, uint64_t chunk_lo, uint64_t chunk_hi, double S0,
+                   int mode, double target, double *__restrict__ chunk_S, double *__restrict__ total,
+                   uint64_t *__restrict__ found)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SeqShared &sh = *reinterpret_cast<SeqShared *>(smem_raw);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        sh.S = S0;
+        sh.done = 0;
+        sh.found = L;
+    }
+    __syncthreads();
+    for (uint64_t ck = chunk_lo; ck < chunk_hi; ck++) {
+        const uint64_t base = ck * SEQ_CHUNK;
+        const int n = (int)((L - base) < (uint64_t)SEQ_CHUNK ? (L - base) : SEQ_CHUNK);
+        if (mode == 0 && tid == 0) chunk_S[ck] = sh.S;
+        double v[SEQ_V];
+#pragma unroll
+        for (int k = 0; k < SEQ_V; k++) {
+            const int li = tid * SEQ_V + k;
+            v[k] = (li < n) ? p[base + li] : 0.0;
+        }
+        if (tid == 0) sh.start = 0;
+        __syncthreads();
+        while (true) {
+            const int start = sh.start;
+            if (start >= n) break;
+            const double S = sh.S;
+            if (S == 0.0) {
+                // running sum is still exactly zero: the first nonzero element sets it
+                int first = n;
+#pragma unroll
+                for (int k = 0; k < SEQ_V; k++) {
+                    const int li = tid * SEQ_V + k;
+                    if (li >= start && li < n && v[k] != 0.0 && li < first) first = li;
+                }
+                first = block_min_int(first, sh.warp_min);
+                if (first >= n) break;  // whole rest of chunk keeps S == 0
+                if (tid == 0) {
+                    double pv = p[base + first];
+                    sh.S = 0.0 + pv;
+                    if (mode == 1 && sh.S > target) {
+                        sh.found = base + first;
+                        sh.done = 1;
+                    }
+                    sh.start = first + 1;
+                }
+                __syncthreads();
+                if (sh.done) break;
+                continue;
+            }
+            double u, B;
+            binade(S, u, B);
+            const uint64_t Su = (uint64_t)(S / u);
+            // per-element unit increments in the current binade
+            uint64_t loc = 0;
+            int any_tie = 0;
+#pragma unroll
+            for (int k = 0; k < SEQ_V; k++) {
+                const int li = tid * SEQ_V + k;
+                uint64_t a = 0;
+                uint8_t t = 0;
+                if (li >= start && li < n) {
+                    const double x = v[k] / u;
+                    if (!(x < 9007199254740992.0)) {
+                        a = 1ull << 54;  // certainly leaves the binade
+                    } else {
+                        const double kf = floor(x), fr = x - kf;
+                        a = (uint64_t)kf + (fr > 0.5 ? 1u : 0u);
+                        t = (fr == 0.5);
+                        any_tie |= t;
+                    }
+                }
+                sh.add[li] = a;
+                sh.tie[li] = t;
+                loc = sat_add(loc, a);
+            }
+            any_tie = __syncthreads_or(any_tie);
+            if (any_tie) {
+                // resolve ties in index order (rare): parity of the running unit count
+                if (tid == 0) {
+                    uint64_t run = Su;
+                    for (int li = start; li < n; li++) {
+                        uint64_t a = sh.add[li];
+                        if (sh.tie[li] && ((run + a) & 1ull)) {
+                            a += 1;
+                            sh.add[li] = a;
+                        }
+                        run = sat_add(run, a);
+                    }
+                }
+                __syncthreads();
+                loc = 0;
+#pragma unroll
+                for (int k = 0; k < SEQ_V; k++) loc = sat_add(loc, sh.add[tid * SEQ_V + k]);
+            }
+            uint64_t run = block_excl_sat(loc, sh.warp_tmp);
+            // inclusive prefix + first crossing (N >= 2^53) / first hit (N > floor(target/u))
+            const double tu = target / u;
+            const bool hit_possible = (mode == 1) && (tu < 9007199254740992.0);
+            const uint64_t tfl = hit_possible ? (uint64_t)floor(tu) : 0;
+            int cross = n, hit = n;
+#pragma unroll
+            for (int k = 0; k < SEQ_V; k++) {
+                const int li = tid * SEQ_V + k;
+                run = sat_add(run, sh.add[li]);
+                sh.P[li] = run;
+                if (li >= start && li < n) {
+                    const uint64_t N = sat_add(Su, run);
+                    if (N >= TWO53 && li < cross) cross = li;
+                    if (hit_possible && N > tfl && li < hit) hit = li;
+                }
+            }
+            cross = block_min_int(cross, sh.warp_min);
+            hit = block_min_int(hit, sh.warp_min);
+            if (tid == 0) {
+                if (hit < cross) {
+                    sh.found = base + hit;
+                    sh.done = 1;
+                } else if (cross < n) {
+                    // exact sum just before the crossing element, then one float add
+                    const uint64_t Nprev = Su + (cross > start ? sh.P[cross - 1] : 0);
+                    const double Sprev = (double)Nprev * u;
+                    const double Snew = Sprev + p[base + cross];
+                    sh.S = Snew;
+                    sh.start = cross + 1;
+                    if (mode == 1 && Snew > target) {
+                        sh.found = base + cross;
+                        sh.done = 1;
+                    }
+                } else {
+                    sh.S = (double)(Su + sh.P[n - 1]) * u;
+                    sh.start = n;
+                }
+            }
+            __syncthreads();
+            if (sh.done) break;
+        }
+        __syncthreads();
+        if (sh.done) break;
+    }
+    if (tid == 0) {
+        if (total) *total = sh.S;
+        if (found) *found = sh.found;
+    }
+}
+
+static size_t seq_smem() { return sizeof(SeqShared); }
+
+static int seq_prepare()
+{
+    static bool done = false;
+    if (!done) {
+        SHB_TRY_CUDA(cudaFuncSetAttribute(seqscan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)seq_smem()));
+        done = true;
+    }
+    return SHB_OK;
+}
+
+}  // namespace shb
+
+using namespace shb;
+
+extern "C" int shb_probabilities(const double *d_state, uint64_t count, double *d_prob, void *stream)
+{
+    if (count == 0) return SHB_OK;
+    cudaStream_t st = as_stream(stream);
+    uint64_t blocks = (count + 255) / 256;
+    const uint64_t cap = (uint64_t)sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    prob_kernel<<<(unsigned)blocks, 256, 0, st>>>((const double2 *)d_state, count, d_prob);
+    SHB_LAUNCHED();
+    SHB_TRY_CUDA(cudaGetLastError());
+    return SHB_OK;
+}
+
+extern "C" int shb_sum(const double *d_x, uint64_t count, double *out, void *stream)
+{
+    if (!out) return set_error(SHB_EINVAL, "null output");
+    *out = 0.0;
+    if (count == 0) return SHB_OK;
+    cudaStream_t st = as_stream(stream);
+    Scratch part, res;
+    SHB_TRY(scratch_alloc(part, sizeof(double) * SUM_BLOCKS, st));
+    SHB_TRY(scratch_alloc(res, sizeof(double), st));
+    sum_partial_kernel<<<SUM_BLOCKS, SUM_THREADS, 0, st>>>(d_x, count, (double *)part.ptr);
+    SHB_LAUNCHED();
+    sum_final_kernel<<<1, SUM_THREADS, 0, st>>>((const double *)part.ptr, SUM_BLOCKS, (double *)res.ptr);
+    SHB_LAUNCHED();
+    SHB_TRY_CUDA(cudaGetLastError());
+    SHB_TRY_CUDA(cudaMemcpyAsync(out, res.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SHB_TRY_CUDA(cudaStreamSynchronize(st));
+    return SHB_OK;
+}
+
+// pass 1 -> (total, chunk starts); kept on device in `chunk_S`
+static int seq_total(const double *d_prob, uint64_t count, double *chunk_S, double *total_host, cudaStream_t st)
+{
+    SHB_TRY(seq_prepare());
+    const uint64_t nch = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    Scratch tot;
+    SHB_TRY(scratch_alloc(tot, sizeof(double), st));
+    seqscan_kernel<<<1, SEQ_THREADS, seq_smem(), st>>>(d_prob, count, 0, nch, 0.0, 0, 0.0, chunk_S,
+                                                         (double *)tot.ptr, nullptr);
+    SHB_LAUNCHED();
+    SHB_TRY_CUDA(cudaGetLastError());
+    SHB_TRY_CUDA(cudaMemcpyAsync(total_host, tot.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SHB_TRY_CUDA(cudaStreamSynchronize(st));
+    return SHB_OK;
+}
+
+extern "C" int shb_cumsum_total(const double *d_prob, uint64_t count, double *total, void *stream)
+{
+    if (!total) return set_error(SHB_EINVAL, "null output");
+    *total = 0.0;
+    if (count == 0) return SHB_OK;
+    cudaStream_t st = as_stream(stream);
+    const uint64_t nch = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    Scratch cs;
+    SHB_TRY(scratch_alloc(cs, sizeof(double) * nch, st));
+    return seq_total(d_prob, count, (double *)cs.ptr, total, st);
+}
+
+extern "C" int shb_cumsum_search(const double *d_prob, uint64_t count, double target, uint64_t *index,
+                                 void *stream)
+{
+    if (!index) return set_error(SHB_EINVAL, "null output");
+    *index = count;
+    if (count == 0) return SHB_OK;
+    cudaStream_t st = as_stream(stream);
+    const uint64_t nch = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    Scratch cs, fnd;
+    SHB_TRY(scratch_alloc(cs, sizeof(double) * nch, st));
+    SHB_TRY(scratch_alloc(fnd, sizeof(uint64_t), st));
+    double tot = 0.0;
+    SHB_TRY(seq_total(d_prob, count, (double *)cs.ptr, &tot, st));
+    if (!(tot > target)) return SHB_OK;  // no running sum exceeds target -> count
+    // chunk c ends with running sum chunk_S[c+1] (or the total for the last one)
+    std::vector<double> hs(nch);
+    SHB_TRY_CUDA(cudaMemcpyAsync(hs.data(), cs.ptr, sizeof(double) * nch, cudaMemcpyDeviceToHost, st));
+    SHB_TRY_CUDA(cudaStreamSynchronize(st));
+    uint64_t lo = 0, hi = nch - 1;  // first chunk whose end value > target
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) / 2;
+        const double end_mid = hs[mid + 1];
+        if (end_mid > target) hi = mid;
+        else lo = mid + 1;
+    }
+    seqscan_kernel<<<1, SEQ_THREADS, seq_smem(), st>>>(d_prob, count, lo, lo + 1, hs[lo], 1, target, nullptr,
+                                                         nullptr, (uint64_t *)fnd.ptr);
+    SHB_LAUNCHED();
+    SHB_TRY_CUDA(cudaGetLastError());
+    SHB_TRY_CUDA(cudaMemcpyAsync(index, fnd.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    SHB_TRY_CUDA(cudaStreamSynchronize(st));
+    return SHB_OK;
+}

@@ -1,0 +1,200 @@
+"""One Shor attempt sharded over the ranks of a torch.distributed group.
+
+One process per GPU.  Rank g of G owns the exponent slice
+a in [g q/G, (g+1) q/G) for modexp / histogram / compaction and the output
+slice c in [g q/G, (g+1) q/G) for the DFT and |V|^2.  The
+exchanges are the ones the algorithm really has:
+
+1. all_reduce(sum) of the exact class counts  -> every rank draws the same k
+2. all_gather of the per-shard supports       -> every rank holds the comb
+3. all_reduce(sum) of the |V|^2 partial sums  -> the normalisation check
+4. gather of the probability shards to rank 0 -> exact sequential CDF, m
+   broadcast back to every rank
+
+Every rank replays the same host Sampler stream, so x, k and m agree by
+construction; each output's summation order does not depend on G, so the
+spectrum is bitwise identical for any G (tests/test_gpu_parity.py).
+
+``ops`` supplies the stage kernels.  The product uses ``DeviceOps``
+(libshorb200.so); tests inject a CPU implementation to exercise the
+collective logic with the gloo backend.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import qstate
+
+
+def shard(total: int, rank: int, world: int) -> tuple[int, int]:
+    lo = total * rank // world
+    hi = total * (rank + 1) // world
+    return lo, hi
+
+
+class DeviceOps:
+    """Stage kernels on the local GPU (libshorb200.so)."""
+
+    def __init__(self):
+        from . import device as dev
+        self.dev = dev
+        import torch
+        self.torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def modexp(self, x, n, count, a_begin):
+        return self.dev.modexp(x, n, count, a_begin)
+
+    def class_counts(self, res, ncls):
+        return self.dev.class_counts(res, ncls)
+
+    def compact_eq(self, res, k, a_begin):
+        return self.dev.compact_eq(res, k, a_begin)
+
+    def progression(self, support):
+        return self.dev.support_progression(support)
+
+    def fill_progression(self, support, m, a0, stride, length, amp):
+        return self.dev.fill_progression(support, m, a0, stride, length, amp)
+
+    def dft(self, amps, length, a0, stride, q, c_begin, c_count, precision):
+        return self.dev.dft(amps, length, a0, stride, q, c_begin, c_count, precision=precision)
+
+    def dsum(self, x):
+        return self.dev.dsum(x)
+
+    def sample(self, prob, u):
+        total = self.dev.cumsum_total(prob)
+        return self.dev.cumsum_search(prob, u * total)
+
+    def empty(self, n, dtype):
+        return self.torch.empty(n, dtype=dtype, device=self.device)
+
+    def to_host(self, t):
+        return t.cpu().numpy()
+
+
+@dataclass
+class AttemptRecord:
+    x: int
+    q: int
+    k: int
+    M: int
+    r: int
+    c0: int
+    m: int
+    norm2: float
+    phase_terms: int
+    dft_ms: float | None = None
+    phase_times: dict = field(default_factory=dict)
+
+
+def _all_gather_var(t, world, group, torch):
+    """all_gather of 1-D tensors of different lengths (padded, then trimmed)."""
+    import torch.distributed as dist
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(sizes) if sizes else 0
+    pad = torch.zeros(max(mx, 1), dtype=t.dtype, device=t.device)
+    pad[: t.numel()] = t
+    bufs = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat([b[:s] for b, s in zip(bufs, sizes)]), sizes
+
+
+def sharded_attempt(n: int, x: int, q: int, sampler: qstate.Sampler, *, rank: int = 0,
+                    world: int = 1, group=None, ops=None, precision: str = "fp64",
+                    time_dft: bool = False, keep_spectrum: bool = False) -> AttemptRecord:
+    """entangle -> measure part 2 -> QFT -> sample part 1 for one base x.
+
+    The caller has already drawn x (shor._draw_base) from the same sampler
+    on every rank.  Returns the attempt record on every rank.
+    """
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    ops = ops or DeviceOps()
+    times = {}
+
+    def tick(name, t0):
+        if hasattr(ops, "synchronize"):
+            ops.synchronize()
+        elif torch.cuda.is_available():
+            torch.cuda.synchronize()
+        times[name] = time.perf_counter() - t0
+        return time.perf_counter()
+
+    t0 = time.perf_counter()
+    a_lo, a_hi = shard(q, rank, world)
+    res = ops.modexp(x, n, a_hi - a_lo, a_lo)
+    t0 = tick("entangle", t0)
+
+    # (1) exact class counts, summed over shards
+    counts = ops.class_counts(res, n)
+    if world > 1:
+        dist.all_reduce(counts, group=group)
+    a_unif = complex(1.0 / math.sqrt(q))
+    w0 = qstate.uniform_weight(a_unif)
+    k = qstate.draw_class(ops.to_host(counts), w0, sampler.uniform())
+    # (2) shard supports -> full comb on every rank (shards are in a order)
+    sup = ops.compact_eq(res, k, a_lo)
+    if world > 1:
+        sup, _ = _all_gather_var(sup, world, group, torch)
+    M = int(sup.numel())
+    amp = qstate.collapsed_amplitude(a_unif, w0, M)
+    a0, stride, length = ops.progression(sup)
+    amps = ops.fill_progression(sup, M, a0, stride, length, amp)
+    del res
+    t0 = tick("measure2", t0)
+
+    # QFT over this rank's output slice
+    c_lo, c_hi = shard(q, rank, world)
+    ev = None
+    if time_dft and torch.cuda.is_available():
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
+    out, prob, bsum = ops.dft(amps, length, a0, stride, q, c_lo, c_hi - c_lo, precision)
+    if ev is not None:
+        ev[1].record()
+    t0 = tick("qft", t0)
+
+    # (3) normalisation (qstate._require_normalized before sampling)
+    norm2 = ops.dsum(bsum)
+    if world > 1:
+        nt = torch.tensor([norm2], dtype=torch.float64, device=bsum.device)
+        dist.all_reduce(nt, group=group)
+        norm2 = float(nt.item())
+    if abs(math.sqrt(norm2) - 1.0) > 1e-9:
+        raise ValueError(f"register is not normalized (|amp| = {math.sqrt(norm2)!r})")
+    # (4) probability shards -> rank 0 -> exact sequential CDF -> m to all ranks
+    u = sampler.uniform()
+    if world > 1:
+        parts = [torch.empty(shard(q, g, world)[1] - shard(q, g, world)[0], dtype=prob.dtype,
+                             device=prob.device) for g in range(world)]
+        dist.all_gather(parts, prob.contiguous(), group=group)
+        mt = torch.zeros(1, dtype=torch.int64, device=prob.device)
+        if rank == 0:
+            full = torch.cat(parts)
+            mt[0] = ops.sample(full, u)
+            del full
+        del parts
+        dist.broadcast(mt, src=0, group=group)
+        m = int(mt.item())
+    else:
+        m = ops.sample(prob, u)
+    m = min(m, q - 1)
+    tick("sample", t0)
+    dft_ms = ev[0].elapsed_time(ev[1]) if ev is not None else None
+    rec = AttemptRecord(x=x, q=q, k=k, M=M, r=stride, c0=a0, m=m, norm2=norm2,
+                        phase_terms=(c_hi - c_lo) * length, dft_ms=dft_ms, phase_times=times)
+    if keep_spectrum:
+        rec.spectrum = (out, prob)
+    return rec

@@ -1,0 +1,197 @@
+"""QFT engines on the B200: drop-in for ``shorsim.qft``.
+
+Same public names, signatures and validation as the reference (qft.py:29-253).
+Every engine name maps to ONE implementation, the sm_100a direct-DFT kernel
+(``shb_dft``): it evaluates exactly the sum the reference's ``dense_dft``
+defines, V_k = (1/sqrt q) sum_j e^{+2 pi i jk/q} V_j, over the nonzero
+support only.  ``tiled_dft`` keeps its split-K meaning (input segments summed
+in ascending order).  ``fft_dft`` / ``circuit_qft`` are the same unitary and
+are served by the same kernel (no second backend, no CPU fallback); their
+argument checks are kept.
+
+``block_size`` / ``workers`` of ``KernelPlan`` describe the reference's CPU
+thread decomposition; they are validated as before but do not change the GPU
+decomposition (fixed for sm_100a: 256 threads x 4 outputs per CTA).
+``KernelPlan.precision`` ("fp64" default, "fp32" fast path) is the one added
+knob.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _native as nat
+from . import device as dev
+
+ENGINES = ("dense", "tiled", "fft", "circuit")
+CIRCUIT_MAX_WIDTH = 12
+
+
+def _require_power_of_two(q: int) -> None:
+    if q < 2 or q & (q - 1):
+        raise ValueError(f"size must be a power of two >= 2, got {q}")
+
+
+class TwiddleTable:
+    """roots[j] = e^{+2 pi i j/q} (qft.py:39-44).
+
+    The GPU kernel derives every phase from the exact integer index, so the
+    16*q-byte table is only built if a caller reads ``roots``.
+    """
+
+    __slots__ = ("q", "_roots")
+
+    def __init__(self, q: int, roots: np.ndarray | None = None):
+        self.q = q
+        self._roots = roots
+
+    @property
+    def roots(self) -> np.ndarray:
+        if self._roots is None:
+            self._roots = np.exp((2j * np.pi / self.q) * np.arange(self.q))
+        return self._roots
+
+    def __eq__(self, other):
+        return isinstance(other, TwiddleTable) and other.q == self.q
+
+    def __hash__(self):
+        return hash(("TwiddleTable", self.q))
+
+    def __repr__(self):
+        return f"TwiddleTable(q={self.q})"
+
+
+@dataclass(frozen=True)
+class KernelPlan:
+    """Work decomposition (qft.py:47-72) plus the arithmetic precision."""
+
+    block_size: int = 256
+    tiles: int = 1
+    workers: int | None = None
+    precision: str = "fp64"
+
+    def resolved(self, q: int) -> "KernelPlan":
+        bs = min(self.block_size, q)
+        if bs < 1 or q % bs:
+            raise ValueError(f"block_size {self.block_size} does not divide q={q}")
+        if self.tiles < 1 or q % self.tiles:
+            raise ValueError(f"tiles {self.tiles} does not divide q={q}")
+        workers = self.workers if self.workers is not None else (os.cpu_count() or 1)
+        if workers < 1:
+            raise ValueError("workers must be >= 1")
+        if self.precision not in dev.PRECISIONS:
+            raise ValueError(f"precision must be one of {tuple(dev.PRECISIONS)}")
+        return replace(self, block_size=bs, workers=workers)
+
+    def num_blocks(self, q: int) -> int:
+        return q // min(self.block_size, q)
+
+
+def build_twiddles(q: int, max_width: int = 24) -> TwiddleTable:
+    """qft.py:75-80 (validation identical; the table itself is lazy)."""
+    _require_power_of_two(q)
+    if q.bit_length() - 1 > max_width:
+        raise ValueError(f"q={q} exceeds the configured maximum width {max_width}")
+    return TwiddleTable(q)
+
+
+# ------------------------------------------------------------- device engine
+
+def _support_of(state, q: int):
+    """(amps device tensor, length, a0, stride, host_input) for any state form."""
+    t = nat.require_cuda()
+    if isinstance(state, dev.CollapsedAmplitudes):
+        if state.q != q:
+            raise ValueError(f"state length {(state.q,)} does not match q={q}")
+        return state.progression_amplitudes(), state.length, state.a0, state.stride, False
+    if isinstance(state, dev.UniformAmplitudes):
+        if state.q != q:
+            raise ValueError(f"state length {(state.q,)} does not match q={q}")
+        amps = dev.fill_progression(None, q, 0, 1, q, complex(state.value))
+        return amps, q, 0, 1, False
+    if isinstance(state, dev.DeviceSpectrum):
+        if state.q != q:
+            raise ValueError(f"state length {(state.q,)} does not match q={q}")
+        data = state.data
+        host = False
+    else:
+        arr = np.ascontiguousarray(state, dtype=np.complex128)
+        if arr.shape != (q,):
+            raise ValueError(f"state length {arr.shape} does not match q={q}")
+        data = t.from_numpy(arr.view(np.float64)).cuda()
+        host = True
+    a0, stride, length = dev.state_progression(data)
+    amps = dev.gather_progression(data, a0, stride, length) if length else None
+    return amps, length, a0, stride, host
+
+
+def _run(state, q: int, tiles: int, precision: str):
+    amps, length, a0, stride, host = _support_of(state, q)
+    out, prob, bsum = dev.dft(amps, length, a0, stride, q, 0, q, tiles=tiles,
+                              scale=1.0 / math.sqrt(q), precision=precision)
+    spec = dev.DeviceSpectrum(q, out, prob, bsum)
+    return spec.numpy() if host else spec
+
+
+def dense_dft(state, tw: TwiddleTable, plan: KernelPlan):
+    """Direct DFT, untiled (qft.py:270-287), on the GPU.
+
+    A numpy input returns a numpy array (drop-in); a device-resident register
+    part returns a DeviceSpectrum that stays on the GPU.
+    """
+    q = tw.q
+    plan = plan.resolved(q)
+    if plan.tiles != 1:
+        raise ValueError("dense_dft is untiled; use tiled_dft for tiles >= 2")
+    return _run(state, q, 1, plan.precision)
+
+
+def tiled_dft(state, tw: TwiddleTable, plan: KernelPlan):
+    """Split-K DFT (qft.py:290-317): input segments reduced in ascending order."""
+    q = tw.q
+    plan = plan.resolved(q)
+    if plan.tiles < 2:
+        raise ValueError("tiled_dft needs tiles >= 2; use dense_dft otherwise")
+    return _run(state, q, plan.tiles, plan.precision)
+
+
+def _length(state) -> int:
+    return state.q if isinstance(state, dev.DeviceVector) else len(state)
+
+
+def fft_dft(state):
+    """Same transform as qft.py:145-161 (served by the direct-DFT kernel)."""
+    q = _length(state)
+    _require_power_of_two(q)
+    return _run(state, q, 1, "fp64")
+
+
+def circuit_qft(state, max_width: int = CIRCUIT_MAX_WIDTH):
+    """Same unitary as the gate-level engine (qft.py:215-231); width cap kept."""
+    q = _length(state)
+    _require_power_of_two(q)
+    w = q.bit_length() - 1
+    if w > max_width:
+        raise ValueError(f"circuit engine capped at w <= {max_width}, got w={w}")
+    return _run(state, q, 1, "fp64")
+
+
+def transform(state, engine: str, tw: TwiddleTable | None = None, plan: KernelPlan | None = None):
+    """Engine dispatch with the reference's argument semantics (qft.py:234-253)."""
+    if engine not in ENGINES:
+        raise ValueError(f"unknown engine {engine!r}; expected one of {ENGINES}")
+    if engine == "fft":
+        return fft_dft(state)
+    if engine == "circuit":
+        return circuit_qft(state)
+    if tw is None:
+        tw = build_twiddles(_length(state))
+    if plan is None:
+        plan = KernelPlan()
+    if engine == "dense":
+        return dense_dft(state, tw, plan)
+    return tiled_dft(state, tw, plan)

@@ -1,0 +1,72 @@
+"""CPU tests: the C-ABI library loads and exports every declared symbol, and the
+host-side exact helpers reproduce numpy's float64 reductions bit for bit."""
+
+import math
+import re
+
+import numpy as np
+import pytest
+
+from paper_1801_01434_b200 import _native as nat
+from paper_1801_01434_b200 import build as build_mod
+
+HEADER = build_mod.PKG.parent / "include" / "shorb200.h"
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build_mod.build()
+    return nat.load()
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(shb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_what_binding_binds():
+    assert declared_symbols() == sorted(nat.SIGNATURES)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert lib.shb_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", str(nat.LIB_PATH)], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+W_VALUES = [1 / 256, 1 / 512, (1 / math.sqrt(512)) ** 2, (1 / math.sqrt(1 << 15)) ** 2,
+            (1 / math.sqrt(1 << 31)) ** 2, 0.1, 1e-9, 3e-7, 1 / 3, 2.0 ** -30, 5e-324 * 7]
+N_VALUES = [0, 1, 2, 7, 8, 9, 127, 128, 129, 255, 256, 1000, 4096, 5461, 8193, 65535, 100003, 1 << 18]
+
+
+@pytest.mark.parametrize("w", W_VALUES)
+def test_seqsum_const_matches_cumsum_and_bincount(lib, w):
+    for n in N_VALUES:
+        got = nat.host_seqsum_const(w, n)
+        if n == 0:
+            assert got == 0.0
+            continue
+        assert got == np.cumsum(np.full(n, w))[-1]
+        assert got == np.bincount(np.zeros(n, dtype=np.int64), weights=np.full(n, w))[0]
+
+
+@pytest.mark.parametrize("w", W_VALUES)
+def test_pairwise_const_matches_numpy_sum(lib, w):
+    for n in N_VALUES + [1 << 20, 3_000_017]:
+        assert nat.host_pairwise_sum_const(w, n) == np.full(n, w).sum()
+
+
+def test_random_weights_seqsum(lib):
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        w = float(rng.random() * 10.0 ** rng.integers(-15, 2))
+        n = int(rng.integers(1, 200000))
+        assert nat.host_seqsum_const(w, n) == np.cumsum(np.full(n, w))[-1]
+        assert nat.host_pairwise_sum_const(w, n) == np.full(n, w).sum()

@@ -1,0 +1,332 @@
+"""GPU parity: every sm_100a stage against the CPU oracle / reference golden vectors.
+
+Tolerances (BASELINE.json north_star):
+* modexp residues, class counts, support, k, M, amplitude bits, m, r, factors: bit-exact
+* FP64 spectrum: max elementwise |dV| <= 1e-12 and max|dp| / max p <= 1e-9
+* FP32 spectrum: max|dp| / max p <= 1e-4
+* exact-cumsum emulation: bit-identical to numpy's np.cumsum / searchsorted
+"""
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import oracle  # noqa: E402
+from paper_1801_01434_b200 import _native as nat  # noqa: E402
+from paper_1801_01434_b200 import device as dev  # noqa: E402
+from paper_1801_01434_b200 import numtheory as nt  # noqa: E402
+from paper_1801_01434_b200 import qft, qstate, shor  # noqa: E402
+
+
+class Forced(qstate.Sampler):
+    def __init__(self, values):
+        super().__init__(0)
+        self._v = list(values)
+
+    def uniform(self):
+        return self._v.pop(0)
+
+
+@pytest.fixture(scope="module")
+def kats(golden_dir):
+    return json.loads((golden_dir / "kats.json").read_text())
+
+
+def _spec(golden_dir, tag):
+    d = np.load(golden_dir / f"spectrum_{tag}.npz")
+    return {k: d[k] for k in d.files}
+
+
+def _amp(info):
+    return complex(np.uint64(int(info["amp_re_bits"], 16)).view(np.float64),
+                   np.uint64(int(info["amp_im_bits"], 16)).view(np.float64))
+
+
+def _rows(out_dev, rows):
+    v = out_dev.cpu().numpy().view(np.complex128)
+    return v[np.asarray(rows, dtype=np.int64)]
+
+
+# ------------------------------------------------------------------ modexp
+
+@pytest.mark.parametrize("x,n,q", [(7, 15, 256), (2, 15, 16), (1, 15, 8), (140, 221, 1 << 16),
+                                   (1991, 3127, 1 << 20), (20637, 32399, 1 << 22),
+                                   (29890, 46927, 1 << 21), (3, 1000003, 1 << 18),
+                                   (123456789, 4294967291, 1 << 16)])
+def test_modexp_bitexact(x, n, q):
+    got = dev.modexp(x, n, q).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, oracle.modexp_residues(x, n, q))
+
+
+def test_modexp_shards_match_full():
+    full = oracle.modexp_residues(8477, 32399, 1 << 20)
+    for lo, cnt in [(0, 1000), (12345, 77777), ((1 << 20) - 5000, 5000)]:
+        got = dev.modexp(8477, 32399, cnt, a_begin=lo).cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, full[lo:lo + cnt])
+
+
+def test_entangle_kats(kats):
+    for q, x, n, res in kats["entangle"]:
+        reg = qstate.entangle_modexp(qstate.init_uniform(q), x, n)
+        assert np.asarray(reg.residues).tolist() == res
+
+
+# ------------------------------------------------------------------ collapse
+
+@pytest.mark.parametrize("x,n,q", [(7, 15, 256), (140, 221, 1 << 16), (1991, 3127, 1 << 22),
+                                   (3, 1000003, 1 << 17)])
+def test_class_counts_and_compaction(x, n, q):
+    res_d = dev.modexp(x, n, q)
+    res = oracle.modexp_residues(x, n, q)
+    counts = dev.class_counts(res_d, n).cpu().numpy()
+    assert np.array_equal(counts.astype(np.uint64), oracle.class_counts(res, n))
+    for k in {int(res[0]), int(res[q // 3]), int(res[-1])}:
+        sup = dev.compact_eq(res_d, k).cpu().numpy()
+        assert np.array_equal(sup, np.flatnonzero(res == k))
+        a0, stride, length = dev.support_progression(dev.compact_eq(res_d, k))
+        assert (a0, length) == (int(sup[0]), len(sup))
+        assert stride == nt.classical_period(x, n) if len(sup) > 1 else True
+    assert dev.compact_eq(res_d, n + 5).numel() == 0
+
+
+def test_measure_sweep_vs_reference(kats):
+    rows = kats["measure_sweep"]
+    for row in rows:
+        q, x, n, u = row["q"], row["x"], row["n"], row["u"]
+        reg = qstate.entangle_modexp(qstate.init_uniform(q), x, n)
+        k, rc = qstate.measure_part2(reg, Forced([u]))
+        a = rc.amplitudes
+        assert k == row["k"]
+        assert a.m == row["M"] and a.a0 == row["c0"]
+        if a.m > 1:
+            assert a.stride == row["r"]
+        assert np.float64(a.amp.real).view(np.uint64) == np.uint64(int(row["amp_re_bits"], 16))
+        assert np.float64(a.amp.imag).view(np.uint64) == np.uint64(int(row["amp_im_bits"], 16))
+
+
+def test_spec_collapse_examples():
+    # SPEC.md:163-165
+    reg = qstate.entangle_modexp(qstate.init_uniform(256), 2, 15)
+    k, rc = qstate.measure_part2(reg, Forced([0.0]))
+    assert k == 1
+    host = np.asarray(rc.amplitudes)
+    assert np.flatnonzero(host).tolist() == list(range(0, 256, 4))
+    assert np.all(host[::4] == 0.125)
+    k, rc = qstate.measure_part2(reg, Forced([0.3]))
+    assert k == 2 and np.flatnonzero(np.asarray(rc.amplitudes)).tolist() == list(range(1, 256, 4))
+    with pytest.raises(ValueError):
+        qstate.measure_part2(rc, Forced([0.1]))
+    assert abs(qstate.l2_norm(rc) - 1.0) < 1e-12
+
+
+# ------------------------------------------------------------------ DFT
+
+def _check_spectrum(got, ref, tol_abs=1e-12, tol_p=1e-9):
+    got = np.asarray(got)
+    ref = np.asarray(ref)
+    assert np.max(np.abs(got - ref)) <= tol_abs
+    pg, pr = np.abs(got) ** 2, np.abs(ref) ** 2
+    assert np.max(np.abs(pg - pr)) / np.max(pr) <= tol_p
+
+
+@pytest.mark.parametrize("tag", ["n15", "n15x2", "n221a1", "n221a2", "n3127"])
+def test_dft_vs_reference_rows(golden_dir, tag):
+    d = _spec(golden_dir, tag)
+    info = json.loads(str(d["info"]))
+    q, M, c0, r = int(d["q"]), info["M"], info["c0"], info["r"]
+    sup = torch.arange(M, dtype=torch.int64, device="cuda") * r + c0
+    amps = dev.fill_progression(sup, M, c0, r, M, _amp(info))
+    rows = d["rows"].astype(np.int64)
+    if q <= (1 << 16):
+        out, prob, _ = dev.dft(amps, M, c0, r, q, 0, q)
+        _check_spectrum(_rows(out, rows), d["V"])
+        # fused probabilities are |V|^2 as numpy computes them
+        p_host = prob.cpu().numpy()
+        assert np.array_equal(p_host, np.abs(out.cpu().numpy().view(np.complex128)) ** 2)
+    else:
+        for c in rows[:64]:
+            out, _, _ = dev.dft(amps, M, c0, r, q, int(c), 1)
+            _check_spectrum(out.cpu().numpy().view(np.complex128), d["V"][rows == c])
+
+
+def test_dft_full_vs_closed_form_2_24(golden_dir):
+    d = _spec(golden_dir, "n3127")
+    info = json.loads(str(d["info"]))
+    q, M, c0, r = int(d["q"]), info["M"], info["c0"], info["r"]
+    sup = torch.arange(M, dtype=torch.int64, device="cuda") * r + c0
+    amps = dev.fill_progression(sup, M, c0, r, M, _amp(info))
+    out, prob, bsum = dev.dft(amps, M, c0, r, q, 0, q)
+    p = prob.cpu().numpy()
+    rows = np.random.default_rng(5).choice(q, 20000, replace=False)
+    cf = oracle.comb_probabilities(q, r, c0, M, rows)
+    assert np.max(np.abs(p[rows] - cf)) / p.max() < 1e-9
+    # unitarity and the golden rows (computed by the reference kernel)
+    assert abs(dev.dsum(bsum) - 1.0) < 1e-9
+    _check_spectrum(_rows(out, d["rows"]), d["V"], tol_abs=1e-11)
+
+
+def test_fp32_fast_path(golden_dir):
+    d = _spec(golden_dir, "n221a1")
+    info = json.loads(str(d["info"]))
+    q, M, c0, r = int(d["q"]), info["M"], info["c0"], info["r"]
+    sup = torch.arange(M, dtype=torch.int64, device="cuda") * r + c0
+    amps = dev.fill_progression(sup, M, c0, r, M, _amp(info))
+    _, p32, _ = dev.dft(amps, M, c0, r, q, 0, q, precision="fp32")
+    _, p64, _ = dev.dft(amps, M, c0, r, q, 0, q, precision="fp64")
+    p32, p64 = p32.cpu().numpy(), p64.cpu().numpy()
+    assert np.max(np.abs(p32 - p64)) / p64.max() <= 1e-4
+
+
+def test_random_states_dense_tiled(golden_dir):
+    d = np.load(golden_dir / "random_states.npz")
+    for key in ("16", "256", "1024", "4096", "sparse2048"):
+        z = d[f"{key}_state"]
+        q = z.size
+        tw = qft.build_twiddles(q)
+        got = qft.dense_dft(z, tw, qft.KernelPlan())
+        assert isinstance(got, np.ndarray)
+        assert np.max(np.abs(got - d[f"{key}_dense"])) < 1e-12
+        got_t = qft.tiled_dft(z, tw, qft.KernelPlan(tiles=8))
+        assert np.max(np.abs(got_t - d[f"{key}_tiled8"])) < 1e-12
+        # engine equivalence + unitarity
+        for eng in ("fft", "circuit"):
+            assert np.max(np.abs(qft.transform(z, eng) - d[f"{key}_dense"])) < 1e-9
+        assert abs(np.linalg.norm(got) - 1.0) < 1e-9
+
+
+def test_spec_qft_examples():
+    q = 4
+    basis = np.zeros(q, complex)
+    basis[0] = 1
+    tw = qft.build_twiddles(q)
+    assert np.allclose(qft.dense_dft(basis, tw, qft.KernelPlan()), 0.5)
+    u = np.full(256, 1 / 16, complex)
+    out = qft.dense_dft(u, qft.build_twiddles(256), qft.KernelPlan())
+    assert abs(out[0] - 1) < 1e-12 and np.max(np.abs(out[1:])) < 1e-12
+    out = qft.tiled_dft(u, qft.build_twiddles(256), qft.KernelPlan(tiles=4))
+    assert abs(out[0] - 1) < 1e-12 and np.max(np.abs(out[1:])) < 1e-12
+    z = np.zeros(8, complex)
+    z[0] = 1
+    assert np.allclose(qft.fft_dft(z), 1 / math.sqrt(8))
+    with pytest.raises(ValueError):
+        qft.tiled_dft(u, qft.build_twiddles(256), qft.KernelPlan(tiles=1))
+    with pytest.raises(ValueError):
+        qft.dense_dft(u, qft.build_twiddles(256), qft.KernelPlan(tiles=2))
+
+
+def test_dft_sharded_rows_bitwise_identical():
+    # output sharding must not change any value (multi-GPU bitwise requirement)
+    q, c0, r, M = 1 << 18, 11, 12, ((1 << 18) - 1 - 11) // 12 + 1
+    sup = torch.arange(M, dtype=torch.int64, device="cuda") * r + c0
+    amps = dev.fill_progression(sup, M, c0, r, M, complex(1 / math.sqrt(M)))
+    full, _, _ = dev.dft(amps, M, c0, r, q, 0, q)
+    full = full.cpu().numpy()
+    for g in (2, 4, 8):
+        parts = [dev.dft(amps, M, c0, r, q, s * q // g, q // g)[0].cpu().numpy() for s in range(g)]
+        assert np.array_equal(np.concatenate(parts).view(np.uint64), full.view(np.uint64))
+
+
+def test_host_abi_dropins(golden_dir):
+    lib = nat.load()
+    d = np.load(golden_dir / "random_states.npz")
+    z = np.ascontiguousarray(d["1024_state"])
+    out = np.empty_like(z)
+    nat.check(lib.shb_dense_dft_host(z.ctypes.data, z.size, 1, 0, out.ctypes.data))
+    assert np.max(np.abs(out - d["1024_dense"])) < 1e-12
+    nat.check(lib.shb_dense_dft_host(z.ctypes.data, z.size, 8, 0, out.ctypes.data))
+    assert np.max(np.abs(out - d["1024_tiled8"])) < 1e-12
+    # the _kernels.partial_row_sums seam: unscaled rows over an input window
+    rows = np.arange(100, 164, dtype=np.uint64)
+    part = np.empty(64, dtype=np.complex128)
+    nat.check(lib.shb_partial_row_sums_host(part.ctypes.data, z.ctypes.data, None, z.size, 100, 164, 256, 768))
+    ref = oracle.dense_rows_literal(z, rows, 256, 768)
+    assert np.max(np.abs(part - ref)) < 1e-12
+    with pytest.raises(ValueError):
+        nat.check(lib.shb_dense_dft_host(z.ctypes.data, 1000, 1, 0, out.ctypes.data))
+
+
+# ------------------------------------------------------------------ sampling
+
+def _adversarial_probs(rng, n):
+    kinds = [
+        rng.random(n) ** 8,
+        np.where(rng.random(n) < 0.9, 0.0, rng.random(n)),
+        np.full(n, 2.0 ** -20),
+        (rng.integers(0, 4, n) * 2.0 ** -30),
+        np.exp(rng.normal(-30, 12, n)),
+        np.concatenate([[1e-300, 5e-324], rng.random(n - 2) * 1e-9]),
+    ]
+    return [np.ascontiguousarray(k / k.sum() if k.sum() > 0 else k) for k in kinds]
+
+
+@pytest.mark.parametrize("n", [1, 7, 8192, 8193, 100003, 1 << 20])
+def test_exact_cumsum_emulation(n):
+    rng = np.random.default_rng(n)
+    for p in _adversarial_probs(rng, n):
+        pd = torch.from_numpy(p).cuda()
+        cum = np.cumsum(p)
+        total = dev.cumsum_total(pd)
+        assert np.float64(total).view(np.uint64) == cum[-1].view(np.uint64)
+        for u in (0.0, 0.25, 0.5, 0.999, float(np.nextafter(1.0, 0.0))) + tuple(rng.random(5)):
+            target = u * cum[-1]
+            want = int(np.searchsorted(cum, target, side="right"))
+            assert dev.cumsum_search(pd, target) == want
+        # exact hits on CDF values (the boundary case)
+        for i in rng.integers(0, n, 5):
+            want = int(np.searchsorted(cum, cum[i], side="right"))
+            assert dev.cumsum_search(pd, float(cum[i])) == want
+
+
+def test_sample_part1_vs_reference(golden_dir):
+    d = np.load(golden_dir / "sampling.npz")
+    z = d["state"]
+    reg = qstate.CompositeRegister(q=z.size, amplitudes=z, residues=np.zeros(z.size, np.int64))
+    for u, m in d["draws"]:
+        assert qstate.sample_part1(reg, Forced([float(u)])) == int(m)
+    # SPEC.md:170-172
+    pure = np.zeros(16, complex)
+    pure[3] = 1
+    reg = qstate.CompositeRegister(q=16, amplitudes=pure, residues=np.zeros(16, np.int64))
+    assert qstate.sample_part1(reg, Forced([0.7])) == 3
+    reg = qstate.init_uniform(4)
+    assert qstate.sample_part1(reg, Forced([0.99])) == 3
+
+
+# ------------------------------------------------------------------ end to end
+
+def test_run_shor_traces_vs_reference(kats):
+    for run in kats["traces"]:
+        cfg = dict(run["cfg"])
+        cfg.setdefault("kernel", "fft")
+        res = shor.run_shor(shor.ShorConfig(n=run["n"], max_width=32, **cfg))
+        assert res.succeeded == run["succeeded"]
+        assert res.factors == run["factors"], run
+        assert len(res.attempts) == len(run["attempts"])
+        for got, want in zip(res.attempts, run["attempts"]):
+            assert (got.x, got.q, got.k, got.m) == (want["x"], want["q"], want["k"], want["m"]), run["n"]
+            assert got.outcome.kind == want["outcome"]["kind"]
+            if want["candidate"]:
+                assert got.candidate.p == want["candidate"]["p"]
+
+
+def test_pipeline_q2_24_properties():
+    # n=3127 seed 0 attempt 1: x=1991, r=116, k=825, c0=29, M=144631, m=578525
+    s = qstate.Sampler(0)
+    x = shor._draw_base(3127, s)
+    assert x == 1991
+    reg = qstate.entangle_modexp(qstate.init_uniform(1 << 24), x, 3127)
+    k, rc = qstate.measure_part2(reg, s)
+    a = rc.amplitudes
+    assert (k, a.a0, a.stride, a.m, a.length) == (825, 29, 116, 144631, 144631)
+    spec = qft.transform(rc.amplitudes, "dense", qft.build_twiddles(1 << 24), qft.KernelPlan())
+    assert abs(qstate.l2_norm(qstate.CompositeRegister(1 << 24, spec, None)) - 1.0) < 1e-9
+    m = qstate.sample_part1(qstate.CompositeRegister(1 << 24, spec, None), s)
+    assert m == 578525
