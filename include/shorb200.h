@@ -114,6 +114,16 @@ int shb_dft(const double *d_amps, uint64_t length, uint64_t a0,
             double *d_prob, double *d_block_sums, void *stream);
 uint64_t shb_dft_num_blocks(uint64_t c_count, int precision);
 
+/* Same transform for a uniform comb: every one of the `length` progression
+ * amplitudes equals (amp_re + i amp_im) -- the collapsed register of
+ * measure_part2 (qstate.py:131-134).  The amplitude is factored
+ * out of the sum (out = scale * amp * sum_j e^{...}); no amplitude array. */
+int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, uint64_t a0,
+                    uint64_t stride, uint64_t q, uint64_t c_begin,
+                    uint64_t c_count, uint32_t tiles, double scale,
+                    int precision, double *d_out, double *d_prob,
+                    double *d_block_sums, void *stream);
+
 /* ---------------------------------------------------------------- sampling
  * qstate.sample_part1 / l2_norm (qstate.py:138-148).
  */
@@ -133,6 +143,12 @@ int shb_cumsum_total(const double *d_prob, uint64_t count, double *total,
  * (qstate.py:143): first i with cumsum[i] > target, or count if none. */
 int shb_cumsum_search(const double *d_prob, uint64_t count, double target,
                       uint64_t *index, void *stream);
+
+/* The whole Born-rule read (qstate.py:142-144) for a draw u:
+ * target = u * cumsum[-1], *index = searchsorted(cumsum, target, "right")
+ * (un-clamped; the caller clamps to q-1), *total = cumsum[-1] (nullable). */
+int shb_sample_index(const double *d_prob, uint64_t count, double u,
+                     uint64_t *index, double *total, void *stream);
 
 /* ------------------------------------------------- host-buffer drop-ins
  * These own their device memory (current device) and take HOST buffers:

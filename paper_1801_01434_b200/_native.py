@@ -38,11 +38,14 @@ SIGNATURES = {
     "shb_gather_progression": ([_vp, _u64, _u64, _u64, _vp, _vp], _i32),
     "shb_fill_progression": ([_vp, _u64, _u64, _u64, _u64, _f64, _f64, _vp, _vp], _i32),
     "shb_dft": ([_vp, _u64, _u64, _u64, _u64, _u64, _u64, _u32, _f64, _i32, _vp, _vp, _vp, _vp], _i32),
+    "shb_dft_uniform": ([_f64, _f64, _u64, _u64, _u64, _u64, _u64, _u64, _u32, _f64, _i32, _vp, _vp, _vp, _vp],
+                        _i32),
     "shb_dft_num_blocks": ([_u64, _i32], _u64),
     "shb_probabilities": ([_vp, _u64, _vp, _vp], _i32),
     "shb_sum": ([_vp, _u64, _PF64, _vp], _i32),
     "shb_cumsum_total": ([_vp, _u64, _PF64, _vp], _i32),
     "shb_cumsum_search": ([_vp, _u64, _f64, _P64, _vp], _i32),
+    "shb_sample_index": ([_vp, _u64, _f64, _P64, _PF64, _vp], _i32),
     "shb_dense_dft_host": ([_vp, _u64, _u32, _i32, _vp], _i32),
     "shb_partial_row_sums_host": ([_vp, _vp, _vp, _u64, _u64, _u64, _u64, _u64], _i32),
     "shb_host_seqsum_const": ([_f64, _u64], _f64),

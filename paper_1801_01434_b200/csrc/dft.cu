@@ -12,15 +12,23 @@
 // sincospi), so a segment of the sum is a polynomial in w_c evaluated by
 // Horner's rule in ascending j:
 //
-//   acc <- acc * w_c + amp_j          (4 DFMA = the 8 flops of one phase term)
+//   acc <- acc * w_c + amp_j          (one complex multiply-add per phase term)
 //   segment value = e^{2 pi i a_last c / q} * acc   (exact sincospi re-seed)
 //
 // Segments are re-seeded every SEG terms (rounding growth <= SEG*eps) and
 // tile partials (reference tiles, qft.py:306-316) are added in ascending
-// tile order.  Each thread owns K outputs (K independent FMA chains); the
-// amplitude stream is shared by the whole CTA and staged into shared memory
-// by TMA bulk copies (cp.async.bulk + mbarrier, multi-stage ring), so the
-// inner loop is LDS.128 broadcast + 4K DFMA: FP64-pipe bound.
+// tile order.  Each thread owns K outputs (K independent FMA chains).
+//
+// Two instantiations, selected from the data by the caller:
+//  * generic (UNIF=false): any complex amplitudes.  The amplitude stream is
+//    shared by the whole CTA and staged into shared memory by TMA bulk copies
+//    (cp.async.bulk + mbarrier ring); inner loop = LDS.128 broadcast + 4 DFMA
+//    per output.
+//  * uniform comb (UNIF=true): every amplitude equals `amp` (the collapsed
+//    Shor register).  amp is factored out of the sum, the Horner
+//    step becomes acc*w + 1 (3 DFMA + 1 DMUL, the constant from the constant
+//    bank), which keeps every FP64 instruction at <= 2 register-file operand
+//    reads -- the generic step needs 3 and is register-bandwidth bound.
 //
 // The epilogue fuses |V|^2 (hypot^2, as np.abs(.)**2, qstate.py:141) and a
 // deterministic per-CTA sum of it (norm check, qstate.py:50-53).
@@ -64,12 +72,21 @@ __device__ __forceinline__ void phase(uint64_t idx, uint64_t q, double two_over_
     sincospi((double)sidx * two_over_q, &s, &c);
 }
 
-template <typename R>
-__global__ void __launch_bounds__(DFT_THREADS, 2)
-    dft_kernel(const double2 *__restrict__ amps, const ChunkDesc *__restrict__ sched, uint32_t nchunks,
-               uint64_t a0, uint64_t stride, uint64_t q, double two_over_q, uint64_t c_begin,
-               uint64_t c_count, double scale, double2 *__restrict__ out, double *__restrict__ prob,
-               double *__restrict__ block_sums)
+struct DftArgs {
+    const double2 *amps;
+    const ChunkDesc *sched;
+    uint32_t nchunks;
+    uint64_t a0, stride, q;
+    double two_over_q;
+    uint64_t c_begin, c_count;
+    double out_re, out_im;  // output factor: scale (generic) or scale*amp (uniform)
+    double2 *out;
+    double *prob;
+    double *block_sums;
+};
+
+template <typename R, bool UNIF>
+__global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
 {
     constexpr int K = Prec<R>::K;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -78,62 +95,74 @@ __global__ void __launch_bounds__(DFT_THREADS, 2)
     __shared__ double red_tmp[DFT_THREADS / 32];
 
     const int tid = threadIdx.x;
-    const uint64_t qmask = q - 1;
+    const uint64_t q = p.q, qmask = q - 1;
     const uint64_t cblk = (uint64_t)blockIdx.x * DFT_THREADS * K;
 
-    // per-output state: step rotation w (conj of e^{i phi}), Horner acc,
-    // tile partial t, running total v.
+    // per-output state: step rotation (cos, sin) of phi = 2 pi stride c / q,
+    // Horner acc (h), tile partial (t), running total (v)
     R wr[K], wi[K], hr[K], hi[K];
     double tr[K], ti[K], vr[K], vi[K];
     uint64_t cval[K];
 #pragma unroll
     for (int i = 0; i < K; i++) {
-        const uint64_t ci = cblk + (uint64_t)i * DFT_THREADS + tid;  // offset inside [0, c_count)
-        cval[i] = c_begin + ci;
+        cval[i] = p.c_begin + cblk + (uint64_t)i * DFT_THREADS + tid;
         double co, si;
-        phase((stride * cval[i]) & qmask, q, two_over_q, co, si);
+        phase((p.stride * cval[i]) & qmask, q, p.two_over_q, co, si);
         wr[i] = (R)co;
-        wi[i] = (R)si;  // acc * (co - i si) is done below with +/- signs
+        wi[i] = (R)si;
         hr[i] = hi[i] = (R)0;
         tr[i] = ti[i] = vr[i] = vi[i] = 0.0;
     }
 
-    if (tid == 0) {
+    if (!UNIF) {
+        if (tid == 0) {
 #pragma unroll
-        for (int s = 0; s < DFT_STAGES; s++) mbar_init(&full_bar[s], 1);
-        fence_mbar_init();
+            for (int s = 0; s < DFT_STAGES; s++) mbar_init(&full_bar[s], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
     }
-    __syncthreads();
-
     auto issue = [&](uint32_t ch) {
-        const ChunkDesc d = sched[ch];
+        const ChunkDesc d = p.sched[ch];
         const int s = ch % DFT_STAGES;
         const uint32_t bytes = d.cnt * 16u;
         mbar_arrive_expect_tx(&full_bar[s], bytes);
-        tma_bulk_g2s(buf + (size_t)s * DFT_CHUNK, amps + d.j0, bytes, &full_bar[s]);
+        tma_bulk_g2s(buf + (size_t)s * DFT_CHUNK, p.amps + d.j0, bytes, &full_bar[s]);
     };
-    if (tid == 0) {
-        const uint32_t pro = nchunks < DFT_STAGES ? nchunks : DFT_STAGES;
+    if (!UNIF && tid == 0) {
+        const uint32_t pro = p.nchunks < DFT_STAGES ? p.nchunks : DFT_STAGES;
         for (uint32_t ch = 0; ch < pro; ch++) issue(ch);
     }
 
-    for (uint32_t ch = 0; ch < nchunks; ch++) {
-        const int s = ch % DFT_STAGES;
-        const ChunkDesc d = sched[ch];
-        mbar_wait(&full_bar[s], (ch / DFT_STAGES) & 1u);
-        const double2 *sb = buf + (size_t)s * DFT_CHUNK;
+    for (uint32_t ch = 0; ch < p.nchunks; ch++) {
+        const ChunkDesc d = p.sched[ch];
         const int cnt = (int)d.cnt;
-        int e = 0;
-        for (; e + 4 <= cnt; e += 4) {
+        if (UNIF) {
+            // acc * conj(e^{i phi}) + 1:
+            //   re = acc_re cos + acc_im sin + 1 ; im = acc_im cos - acc_re sin
+#pragma unroll 4
+            for (int e = 0; e < cnt; e++) {
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const double2 av = sb[e + u];
+                for (int i = 0; i < K; i++) {
+                    const R t_re = fma(hi[i], wi[i], (R)1);
+                    const R t_im = hi[i] * wr[i];
+                    const R n_re = fma(hr[i], wr[i], t_re);
+                    const R n_im = fma(-hr[i], wi[i], t_im);
+                    hr[i] = n_re;
+                    hi[i] = n_im;
+                }
+            }
+        } else {
+            const int s = ch % DFT_STAGES;
+            mbar_wait(&full_bar[s], (ch / DFT_STAGES) & 1u);
+            const double2 *sb = buf + (size_t)s * DFT_CHUNK;
+#pragma unroll 4
+            for (int e = 0; e < cnt; e++) {
+                const double2 av = sb[e];
                 const R a_re = (R)av.x, a_im = (R)av.y;
 #pragma unroll
                 for (int i = 0; i < K; i++) {
-                    // acc * conj(e^{i phi}) + a:
-                    //   re = acc_re cos + acc_im sin + a_re
-                    //   im = acc_im cos - acc_re sin + a_im
+                    // acc * conj(e^{i phi}) + a
                     const R t_re = fma(hi[i], wi[i], a_re);
                     const R t_im = fma(hi[i], wr[i], a_im);
                     const R n_re = fma(hr[i], wr[i], t_re);
@@ -143,26 +172,13 @@ __global__ void __launch_bounds__(DFT_THREADS, 2)
                 }
             }
         }
-        for (; e < cnt; e++) {
-            const double2 av = sb[e];
-            const R a_re = (R)av.x, a_im = (R)av.y;
-#pragma unroll
-            for (int i = 0; i < K; i++) {
-                const R t_re = fma(hi[i], wi[i], a_re);
-                const R t_im = fma(hi[i], wr[i], a_im);
-                const R n_re = fma(hr[i], wr[i], t_re);
-                const R n_im = fma(-hr[i], wi[i], t_im);
-                hr[i] = n_re;
-                hi[i] = n_im;
-            }
-        }
         if (d.flags & CH_SEG_END) {
             // seed = e^{+2 pi i a_last c / q}; t += seed * acc; acc = 0
-            const uint64_t a_last = a0 + (d.j0 + d.cnt - 1) * stride;
+            const uint64_t a_last = p.a0 + (d.j0 + d.cnt - 1) * p.stride;
 #pragma unroll
             for (int i = 0; i < K; i++) {
                 double sc, ss;
-                phase((a_last * cval[i]) & qmask, q, two_over_q, sc, ss);
+                phase((a_last * cval[i]) & qmask, q, p.two_over_q, sc, ss);
                 const double xr = (double)hr[i], xi = (double)hi[i];
                 tr[i] = fma(sc, xr, fma(-ss, xi, tr[i]));
                 ti[i] = fma(sc, xi, fma(ss, xr, ti[i]));
@@ -177,25 +193,28 @@ __global__ void __launch_bounds__(DFT_THREADS, 2)
                 tr[i] = ti[i] = 0.0;
             }
         }
-        __syncthreads();  // every warp is done with stage s
-        if (tid == 0 && ch + DFT_STAGES < nchunks) issue(ch + DFT_STAGES);
+        if (!UNIF) {
+            __syncthreads();  // every warp is done with stage s
+            if (tid == 0 && ch + DFT_STAGES < p.nchunks) issue(ch + DFT_STAGES);
+        }
     }
 
-    // epilogue: scale (out *= 1/sqrt(q), qft.py:286), |V|^2, block sum
+    // epilogue: output factor (1/sqrt(q), times amp on the uniform path), |V|^2, block sum
     double psum = 0.0;
 #pragma unroll
     for (int i = 0; i < K; i++) {
         const uint64_t ci = cblk + (uint64_t)i * DFT_THREADS + tid;
-        if (ci < c_count) {
-            const double o_re = vr[i] * scale, o_im = vi[i] * scale;
-            out[ci] = make_double2(o_re, o_im);
+        if (ci < p.c_count) {
+            const double o_re = vr[i] * p.out_re - vi[i] * p.out_im;
+            const double o_im = vr[i] * p.out_im + vi[i] * p.out_re;
+            p.out[ci] = make_double2(o_re, o_im);
             const double h = hypot(o_re, o_im);
-            const double p = h * h;
-            if (prob) prob[ci] = p;
-            psum += p;
+            const double pr = h * h;
+            if (p.prob) p.prob[ci] = pr;
+            psum += pr;
         }
     }
-    if (block_sums) {
+    if (p.block_sums) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) psum += __shfl_down_sync(0xffffffffu, psum, o);
         if ((tid & 31) == 0) red_tmp[tid >> 5] = psum;
@@ -204,27 +223,26 @@ __global__ void __launch_bounds__(DFT_THREADS, 2)
             double b = 0.0;
 #pragma unroll
             for (int w = 0; w < DFT_THREADS / 32; w++) b += red_tmp[w];
-            block_sums[blockIdx.x] = b;
+            p.block_sums[blockIdx.x] = b;
         }
     }
 }
 
-template <typename R>
-static int launch_dft(const double *d_amps, uint64_t length, uint64_t a0, uint64_t stride, uint64_t q,
-                      uint64_t c_begin, uint64_t c_count, uint32_t tiles, double scale, double *d_out,
-                      double *d_prob, double *d_block_sums, cudaStream_t st)
+template <typename R, bool UNIF>
+static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t st)
 {
     constexpr int K = Prec<R>::K;
     const uint64_t SEG = Prec<R>::SEG;
+    const uint64_t q = a.q, a0 = a.a0, stride = a.stride;
     // ---- chunk schedule: tiles -> re-seed segments -> smem chunks
     std::vector<ChunkDesc> sched;
     sched.reserve(length / DFT_CHUNK + tiles + length / SEG + 4);
     const uint64_t tile_span = q / tiles;
     for (uint32_t t = 0; t < tiles && length; t++) {
         const uint64_t lo_a = (uint64_t)t * tile_span, hi_a = lo_a + tile_span;
-        auto first_j_at_or_above = [&](uint64_t a) -> uint64_t {
-            if (a <= a0) return 0;
-            const uint64_t j = (a - a0 + stride - 1) / stride;
+        auto first_j_at_or_above = [&](uint64_t x) -> uint64_t {
+            if (x <= a0) return 0;
+            const uint64_t j = (x - a0 + stride - 1) / stride;
             return j < length ? j : length;
         };
         const uint64_t jlo = first_j_at_or_above(lo_a), jhi = first_j_at_or_above(hi_a);
@@ -240,27 +258,57 @@ static int launch_dft(const double *d_amps, uint64_t length, uint64_t a0, uint64
             }
         }
     }
-    const uint32_t nchunks = (uint32_t)sched.size();
+    a.nchunks = (uint32_t)sched.size();
     Scratch d_sched;
-    SHB_TRY(scratch_alloc(d_sched, sizeof(ChunkDesc) * (nchunks ? nchunks : 1), st));
-    if (nchunks)
-        SHB_TRY_CUDA(cudaMemcpyAsync(d_sched.ptr, sched.data(), sizeof(ChunkDesc) * nchunks,
+    SHB_TRY(scratch_alloc(d_sched, sizeof(ChunkDesc) * (a.nchunks ? a.nchunks : 1), st));
+    if (a.nchunks)
+        SHB_TRY_CUDA(cudaMemcpyAsync(d_sched.ptr, sched.data(), sizeof(ChunkDesc) * a.nchunks,
                                      cudaMemcpyHostToDevice, st));
-    const size_t smem = (size_t)DFT_STAGES * DFT_CHUNK * sizeof(double2);
+    a.sched = (const ChunkDesc *)d_sched.ptr;
+    const size_t smem = UNIF ? 0 : (size_t)DFT_STAGES * DFT_CHUNK * sizeof(double2);
     static bool attr_done = false;
-    if (!attr_done) {
-        SHB_TRY_CUDA(cudaFuncSetAttribute(dft_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (!attr_done && smem) {
+        SHB_TRY_CUDA(cudaFuncSetAttribute(dft_kernel<R, UNIF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
         attr_done = true;
     }
     const uint64_t per_blk = (uint64_t)DFT_THREADS * K;
-    const uint64_t nblk = (c_count + per_blk - 1) / per_blk;
+    const uint64_t nblk = (a.c_count + per_blk - 1) / per_blk;
     if (nblk > 0x7FFFFFFFull) return set_error(SHB_EINVAL, "too many outputs for one launch");
-    dft_kernel<R><<<(unsigned)nblk, DFT_THREADS, smem, st>>>(
-        (const double2 *)d_amps, (const ChunkDesc *)d_sched.ptr, nchunks, a0, stride, q, 2.0 / (double)q,
-        c_begin, c_count, scale, (double2 *)d_out, d_prob, d_block_sums);
+    dft_kernel<R, UNIF><<<(unsigned)nblk, DFT_THREADS, smem, st>>>(a);
     SHB_LAUNCHED();
     SHB_TRY_CUDA(cudaGetLastError());
     return SHB_OK;
+}
+
+static int validate(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin,
+                    uint64_t c_count, uint32_t tiles, int precision, double *d_out)
+{
+    if (q < 2 || (q & (q - 1))) return set_error(SHB_EINVAL, "q must be a power of two >= 2");
+    if (tiles < 1 || q % tiles) return set_error(SHB_EINVAL, "tiles %u does not divide q", tiles);
+    if (stride == 0) return set_error(SHB_EINVAL, "stride must be >= 1");
+    if (c_begin > q || c_count > q - c_begin) return set_error(SHB_EINVAL, "output rows outside [0, q)");
+    if (length && (a0 >= q || (length - 1) > (q - 1 - a0) / stride))
+        return set_error(SHB_EINVAL, "support progression leaves [0, q)");
+    if (precision != SHB_FP64 && precision != SHB_FP32) return set_error(SHB_EINVAL, "unknown precision %d", precision);
+    if (c_count && !d_out) return set_error(SHB_EINVAL, "null output buffer");
+    return SHB_OK;
+}
+
+static DftArgs make_args(uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin, uint64_t c_count,
+                         double *d_out, double *d_prob, double *d_block_sums)
+{
+    DftArgs a{};
+    a.a0 = a0;
+    a.stride = stride;
+    a.q = q;
+    a.two_over_q = 2.0 / (double)q;
+    a.c_begin = c_begin;
+    a.c_count = c_count;
+    a.out = (double2 *)d_out;
+    a.prob = d_prob;
+    a.block_sums = d_block_sums;
+    return a;
 }
 
 }  // namespace shb
@@ -278,22 +326,31 @@ extern "C" int shb_dft(const double *d_amps, uint64_t length, uint64_t a0, uint6
                        uint64_t c_begin, uint64_t c_count, uint32_t tiles, double scale, int precision,
                        double *d_out, double *d_prob, double *d_block_sums, void *stream)
 {
-    if (q < 2 || (q & (q - 1))) return set_error(SHB_EINVAL, "q must be a power of two >= 2");
-    if (tiles < 1 || q % tiles) return set_error(SHB_EINVAL, "tiles %u does not divide q", tiles);
-    if (stride == 0) return set_error(SHB_EINVAL, "stride must be >= 1");
-    if (c_begin > q || c_count > q - c_begin) return set_error(SHB_EINVAL, "output rows outside [0, q)");
-    if (length && (a0 >= q || (length - 1) > (q - 1 - a0) / stride))
-        return set_error(SHB_EINVAL, "support progression leaves [0, q)");
-    if (precision != SHB_FP64 && precision != SHB_FP32) return set_error(SHB_EINVAL, "unknown precision %d", precision);
+    SHB_TRY(validate(length, a0, stride, q, c_begin, c_count, tiles, precision, d_out));
     if (c_count == 0) return SHB_OK;
-    if (!d_out) return set_error(SHB_EINVAL, "null output buffer");
     if (length && !d_amps) return set_error(SHB_EINVAL, "null amplitude buffer");
     if (length && (reinterpret_cast<uintptr_t>(d_amps) & 15))
         return set_error(SHB_EINVAL, "amplitude buffer must be 16-byte aligned");
+    DftArgs a = make_args(a0, stride, q, c_begin, c_count, d_out, d_prob, d_block_sums);
+    a.amps = (const double2 *)d_amps;
+    a.out_re = scale;
+    a.out_im = 0.0;
     cudaStream_t st = as_stream(stream);
-    if (precision == SHB_FP32)
-        return launch_dft<float>(d_amps, length, a0, stride, q, c_begin, c_count, tiles, scale, d_out, d_prob,
-                                 d_block_sums, st);
-    return launch_dft<double>(d_amps, length, a0, stride, q, c_begin, c_count, tiles, scale, d_out, d_prob,
-                              d_block_sums, st);
+    if (precision == SHB_FP32) return launch_dft<float, false>(a, length, tiles, st);
+    return launch_dft<double, false>(a, length, tiles, st);
+}
+
+extern "C" int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, uint64_t a0, uint64_t stride,
+                               uint64_t q, uint64_t c_begin, uint64_t c_count, uint32_t tiles, double scale,
+                               int precision, double *d_out, double *d_prob, double *d_block_sums, void *stream)
+{
+    SHB_TRY(validate(length, a0, stride, q, c_begin, c_count, tiles, precision, d_out));
+    if (c_count == 0) return SHB_OK;
+    DftArgs a = make_args(a0, stride, q, c_begin, c_count, d_out, d_prob, d_block_sums);
+    a.amps = nullptr;
+    a.out_re = amp_re * scale;
+    a.out_im = amp_im * scale;
+    cudaStream_t st = as_stream(stream);
+    if (precision == SHB_FP32) return launch_dft<float, true>(a, length, tiles, st);
+    return launch_dft<double, true>(a, length, tiles, st);
 }

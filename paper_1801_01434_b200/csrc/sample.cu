@@ -160,152 +160,320 @@ __device__ inline int block_min_int(int v, uint32_t *warp_min)
     return r;
 }
 
-// Walk chunks [chunk_lo, chunk_hi) of p starting from the exact running sum
-// S0.  mode 0: record S at every chunk start (chunk_S) and the total.
+// Per-tile record for the fast walk: integer increment of the whole tile in
+// the binade predicted for its start (approximate prefix of tile sums).
+struct TileRec {
+    uint64_t A;     // sum over the tile of round(p / 2^uexp) (saturating)
+    int32_t uexp;   // predicted ulp exponent (INT32_MIN: predicted start sum is 0)
+    uint32_t flags; // TR_TIES | TR_ALLZERO
+};
+enum : uint32_t { TR_TIES = 1u, TR_ALLZERO = 2u };
+
+__device__ __forceinline__ int ulp_exp(double S)
+{
+    if (S < 0x1p-1021) return -1074;
+    int e;
+    frexp(S, &e);
+    return e - 53;
+}
+
+// pass 1: approximate tile sums (any order: they only predict binades)
+__global__ void __launch_bounds__(256) tile_sum_kernel(const double *__restrict__ p, uint64_t L,
+                                                      double *__restrict__ tsum)
+{
+    __shared__ double tmp[8];
+    const uint64_t base = (uint64_t)blockIdx.x * SEQ_CHUNK;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < SEQ_CHUNK; i += 256)
+        if (base + i < L) s += p[base + i];
+    const double b = block_sum(s, tmp);
+    if (threadIdx.x == 0) tsum[blockIdx.x] = b;
+}
+
+// pass 2: exclusive prefix of the tile sums (one CTA)
+__global__ void __launch_bounds__(SUM_THREADS) tile_prefix_kernel(const double *__restrict__ tsum, uint64_t nt,
+                                                                 double *__restrict__ tstart)
+{
+    __shared__ double part[SUM_THREADS];
+    const uint64_t per = (nt + SUM_THREADS - 1) / SUM_THREADS;
+    const uint64_t lo = per * threadIdx.x, hi = lo + per < nt ? lo + per : nt;
+    double s = 0.0;
+    for (uint64_t i = lo; i < hi; i++) s += tsum[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double run = 0.0;
+        for (int t = 0; t < SUM_THREADS; t++) {
+            const double v = part[t];
+            part[t] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    double run = part[threadIdx.x];
+    for (uint64_t i = lo; i < hi; i++) {
+        tstart[i] = run;
+        run += tsum[i];
+    }
+}
+
+// pass 3: per-tile integer increment in the predicted binade
+__global__ void __launch_bounds__(256) tile_rec_kernel(const double *__restrict__ p, uint64_t L,
+                                                      const double *__restrict__ tstart,
+                                                      TileRec *__restrict__ rec)
+{
+    __shared__ uint64_t tmpA[8];
+    __shared__ uint32_t tmpF[8];
+    const uint64_t base = (uint64_t)blockIdx.x * SEQ_CHUNK;
+    const double S0 = tstart[blockIdx.x];
+    const bool zero = !(S0 > 0.0);
+    const int ue = zero ? -1074 : ulp_exp(S0);
+    uint64_t A = 0;
+    uint32_t ties = 0, nonzero = 0;
+    for (int i = threadIdx.x; i < SEQ_CHUNK; i += 256) {
+        if (base + i >= L) break;
+        const double v = p[base + i];
+        nonzero |= (v != 0.0);
+        const double x = ldexp(v, -ue);  // exact power-of-two scaling
+        uint64_t a;
+        if (!(x < 9007199254740992.0)) {
+            a = 1ull << 54;
+        } else {
+            const double kf = floor(x), fr = x - kf;
+            a = (uint64_t)kf + (fr > 0.5 ? 1u : 0u);
+            ties |= (fr == 0.5);
+        }
+        A = sat_add(A, a);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        A = sat_add(A, __shfl_down_sync(0xffffffffu, A, o));
+        ties |= __shfl_down_sync(0xffffffffu, ties, o);
+        nonzero |= __shfl_down_sync(0xffffffffu, nonzero, o);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        tmpA[wid] = A;
+        tmpF[wid] = (ties ? TR_TIES : 0u) | (nonzero ? 0u : TR_ALLZERO);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t a = 0;
+        uint32_t f = TR_ALLZERO;
+        for (int w = 0; w < 8; w++) {
+            a = sat_add(a, tmpA[w]);
+            const uint32_t fw = tmpF[w];
+            f = (f & fw & TR_ALLZERO) | ((f | fw) & TR_TIES);
+        }
+        rec[blockIdx.x] = TileRec{a, zero ? INT32_MIN : ue, f};
+    }
+}
+
+// Detailed exact walk of one tile by the whole CTA (binade crossings, ties,
+// first nonzero, or the target search).  Updates sh.S / sh.found / sh.done.
+__device__ void walk_tile(const double *__restrict__ p, uint64_t L, uint64_t ck, int mode, double target,
+                          SeqShared &sh)
+{
+    const int tid = threadIdx.x;
+    const uint64_t base = ck * SEQ_CHUNK;
+    const int n = (int)((L - base) < (uint64_t)SEQ_CHUNK ? (L - base) : SEQ_CHUNK);
+    double v[SEQ_V];
+#pragma unroll
+    for (int k = 0; k < SEQ_V; k++) {
+        const int li = tid * SEQ_V + k;
+        v[k] = (li < n) ? p[base + li] : 0.0;
+    }
+    if (tid == 0) sh.start = 0;
+    __syncthreads();
+    while (true) {
+        const int start = sh.start;
+        if (start >= n) break;
+        const double S = sh.S;
+        if (S == 0.0) {
+            // running sum is still exactly zero: the first nonzero element sets it
+            int first = n;
+#pragma unroll
+            for (int k = 0; k < SEQ_V; k++) {
+                const int li = tid * SEQ_V + k;
+                if (li >= start && li < n && v[k] != 0.0 && li < first) first = li;
+            }
+            first = block_min_int(first, sh.warp_min);
+            if (first >= n) break;  // whole rest of the tile keeps S == 0
+            if (tid == 0) {
+                sh.S = 0.0 + p[base + first];
+                if (mode == 1 && sh.S > target) {
+                    sh.found = base + first;
+                    sh.done = 1;
+                }
+                sh.start = first + 1;
+            }
+            __syncthreads();
+            if (sh.done) break;
+            continue;
+        }
+        double u, B;
+        binade(S, u, B);
+        const uint64_t Su = (uint64_t)(S / u);
+        // per-element unit increments in the current binade
+        uint64_t loc = 0;
+        int any_tie = 0;
+#pragma unroll
+        for (int k = 0; k < SEQ_V; k++) {
+            const int li = tid * SEQ_V + k;
+            uint64_t a = 0;
+            uint8_t t = 0;
+            if (li >= start && li < n) {
+                const double x = v[k] / u;
+                if (!(x < 9007199254740992.0)) {
+                    a = 1ull << 54;  // certainly leaves the binade
+                } else {
+                    const double kf = floor(x), fr = x - kf;
+                    a = (uint64_t)kf + (fr > 0.5 ? 1u : 0u);
+                    t = (fr == 0.5);
+                    any_tie |= t;
+                }
+            }
+            sh.add[li] = a;
+            sh.tie[li] = t;
+            loc = sat_add(loc, a);
+        }
+        any_tie = __syncthreads_or(any_tie);
+        if (any_tie) {
+            // resolve ties in index order (rare): parity of the running unit count
+            if (tid == 0) {
+                uint64_t run = Su;
+                for (int li = start; li < n; li++) {
+                    uint64_t a = sh.add[li];
+                    if (sh.tie[li] && ((run + a) & 1ull)) {
+                        a += 1;
+                        sh.add[li] = a;
+                    }
+                    run = sat_add(run, a);
+                }
+            }
+            __syncthreads();
+            loc = 0;
+#pragma unroll
+            for (int k = 0; k < SEQ_V; k++) loc = sat_add(loc, sh.add[tid * SEQ_V + k]);
+        }
+        uint64_t run = block_excl_sat(loc, sh.warp_tmp);
+        // inclusive prefix + first crossing (N >= 2^53) / first hit (N > floor(target/u))
+        const double tu = target / u;
+        const bool hit_possible = (mode == 1) && (tu < 9007199254740992.0);
+        const uint64_t tfl = hit_possible ? (uint64_t)floor(tu) : 0;
+        int cross = n, hit = n;
+#pragma unroll
+        for (int k = 0; k < SEQ_V; k++) {
+            const int li = tid * SEQ_V + k;
+            run = sat_add(run, sh.add[li]);
+            sh.P[li] = run;
+            if (li >= start && li < n) {
+                const uint64_t N = sat_add(Su, run);
+                if (N >= TWO53 && li < cross) cross = li;
+                if (hit_possible && N > tfl && li < hit) hit = li;
+            }
+        }
+        cross = block_min_int(cross, sh.warp_min);
+        hit = block_min_int(hit, sh.warp_min);
+        if (tid == 0) {
+            if (hit < cross) {
+                sh.found = base + hit;
+                sh.done = 1;
+            } else if (cross < n) {
+                // exact sum just before the crossing element, then one float add
+                const uint64_t Nprev = Su + (cross > start ? sh.P[cross - 1] : 0);
+                const double Sprev = (double)Nprev * u;
+                const double Snew = Sprev + p[base + cross];
+                sh.S = Snew;
+                sh.start = cross + 1;
+                if (mode == 1 && Snew > target) {
+                    sh.found = base + cross;
+                    sh.done = 1;
+                }
+            } else {
+                sh.S = (double)(Su + sh.P[n - 1]) * u;
+                sh.start = n;
+            }
+        }
+        __syncthreads();
+        if (sh.done) break;
+    }
+    __syncthreads();
+}
+
+// Walk tiles [tile_lo, tile_hi) from the exact running sum S0.
+// mode 0: record the exact S at every tile start (tile_S) and the total;
+//         warp 0 advances over tiles whose record proves they stay inside
+//         one binade without ties (S += 2^uexp * A, exact), the whole CTA
+//         walks the others element by element.
 // mode 1: find the first index whose running sum exceeds `target`.
 __global__ void __launch_bounds__(SEQ_THREADS, 1)
-    seqscan_kernel(const double *__restrict__ p, uint64_t L, uint64_t chunk_lo, uint64_t chunk_hi, double S0,
-                   int mode, double target, double *__restrict__ chunk_S, double *__restrict__ total,
-                   uint64_t *__restrict__ found)
+    seqscan_kernel(const double *__restrict__ p, uint64_t L, uint64_t tile_lo, uint64_t tile_hi, double S0,
+                   int mode, double target, const TileRec *__restrict__ recs, double *__restrict__ tile_S,
+                   double *__restrict__ total, uint64_t *__restrict__ found)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SeqShared &sh = *reinterpret_cast<SeqShared *>(smem_raw);
-    const int tid = threadIdx.x;
+    __shared__ uint64_t next_slow;
+    const int tid = threadIdx.x, lane = tid & 31;
     if (tid == 0) {
         sh.S = S0;
         sh.done = 0;
         sh.found = L;
     }
     __syncthreads();
-    for (uint64_t ck = chunk_lo; ck < chunk_hi; ck++) {
-        const uint64_t base = ck * SEQ_CHUNK;
-        const int n = (int)((L - base) < (uint64_t)SEQ_CHUNK ? (L - base) : SEQ_CHUNK);
-        if (mode == 0 && tid == 0) chunk_S[ck] = sh.S;
-        double v[SEQ_V];
-#pragma unroll
-        for (int k = 0; k < SEQ_V; k++) {
-            const int li = tid * SEQ_V + k;
-            v[k] = (li < n) ? p[base + li] : 0.0;
-        }
-        if (tid == 0) sh.start = 0;
-        __syncthreads();
-        while (true) {
-            const int start = sh.start;
-            if (start >= n) break;
-            const double S = sh.S;
-            if (S == 0.0) {
-                // running sum is still exactly zero: the first nonzero element sets it
-                int first = n;
-#pragma unroll
-                for (int k = 0; k < SEQ_V; k++) {
-                    const int li = tid * SEQ_V + k;
-                    if (li >= start && li < n && v[k] != 0.0 && li < first) first = li;
-                }
-                first = block_min_int(first, sh.warp_min);
-                if (first >= n) break;  // whole rest of chunk keeps S == 0
-                if (tid == 0) {
-                    double pv = p[base + first];
-                    sh.S = 0.0 + pv;
-                    if (mode == 1 && sh.S > target) {
-                        sh.found = base + first;
-                        sh.done = 1;
-                    }
-                    sh.start = first + 1;
-                }
-                __syncthreads();
-                if (sh.done) break;
-                continue;
-            }
-            double u, B;
-            binade(S, u, B);
-            const uint64_t Su = (uint64_t)(S / u);
-            // per-element unit increments in the current binade
-            uint64_t loc = 0;
-            int any_tie = 0;
-#pragma unroll
-            for (int k = 0; k < SEQ_V; k++) {
-                const int li = tid * SEQ_V + k;
-                uint64_t a = 0;
-                uint8_t t = 0;
-                if (li >= start && li < n) {
-                    const double x = v[k] / u;
-                    if (!(x < 9007199254740992.0)) {
-                        a = 1ull << 54;  // certainly leaves the binade
-                    } else {
-                        const double kf = floor(x), fr = x - kf;
-                        a = (uint64_t)kf + (fr > 0.5 ? 1u : 0u);
-                        t = (fr == 0.5);
-                        any_tie |= t;
-                    }
-                }
-                sh.add[li] = a;
-                sh.tie[li] = t;
-                loc = sat_add(loc, a);
-            }
-            any_tie = __syncthreads_or(any_tie);
-            if (any_tie) {
-                // resolve ties in index order (rare): parity of the running unit count
-                if (tid == 0) {
-                    uint64_t run = Su;
-                    for (int li = start; li < n; li++) {
-                        uint64_t a = sh.add[li];
-                        if (sh.tie[li] && ((run + a) & 1ull)) {
-                            a += 1;
-                            sh.add[li] = a;
+    uint64_t t = tile_lo;
+    while (t < tile_hi) {
+        if (recs != nullptr) {
+            if (tid < 32) {
+                double S = sh.S;
+                uint64_t tt = t, stop = tile_hi;
+                bool slow = false;
+                while (tt < tile_hi && !slow) {
+                    TileRec r{};
+                    if (tt + lane < tile_hi) r = recs[tt + lane];
+                    const int cnt = (tile_hi - tt) < 32 ? (int)(tile_hi - tt) : 32;
+                    for (int i = 0; i < cnt; i++) {
+                        const uint64_t A = __shfl_sync(0xffffffffu, r.A, i);
+                        const int ue = __shfl_sync(0xffffffffu, r.uexp, i);
+                        const uint32_t fl = __shfl_sync(0xffffffffu, r.flags, i);
+                        double Snew;
+                        bool fast;
+                        if (S == 0.0) {
+                            fast = (fl & TR_ALLZERO) != 0;
+                            Snew = 0.0;
+                        } else {
+                            const int se = ulp_exp(S);
+                            const double u = ldexp(1.0, se);
+                            const uint64_t N = (uint64_t)(S / u) + A;
+                            fast = (se == ue) && !(fl & TR_TIES) && (N < TWO53);
+                            Snew = (double)N * u;
                         }
-                        run = sat_add(run, a);
+                        if (!fast) {
+                            stop = tt + i;
+                            slow = true;
+                            break;
+                        }
+                        if (mode == 0 && lane == 0) tile_S[tt + i] = S;
+                        S = Snew;
                     }
+                    tt += cnt;
                 }
-                __syncthreads();
-                loc = 0;
-#pragma unroll
-                for (int k = 0; k < SEQ_V; k++) loc = sat_add(loc, sh.add[tid * SEQ_V + k]);
-            }
-            uint64_t run = block_excl_sat(loc, sh.warp_tmp);
-            // inclusive prefix + first crossing (N >= 2^53) / first hit (N > floor(target/u))
-            const double tu = target / u;
-            const bool hit_possible = (mode == 1) && (tu < 9007199254740992.0);
-            const uint64_t tfl = hit_possible ? (uint64_t)floor(tu) : 0;
-            int cross = n, hit = n;
-#pragma unroll
-            for (int k = 0; k < SEQ_V; k++) {
-                const int li = tid * SEQ_V + k;
-                run = sat_add(run, sh.add[li]);
-                sh.P[li] = run;
-                if (li >= start && li < n) {
-                    const uint64_t N = sat_add(Su, run);
-                    if (N >= TWO53 && li < cross) cross = li;
-                    if (hit_possible && N > tfl && li < hit) hit = li;
-                }
-            }
-            cross = block_min_int(cross, sh.warp_min);
-            hit = block_min_int(hit, sh.warp_min);
-            if (tid == 0) {
-                if (hit < cross) {
-                    sh.found = base + hit;
-                    sh.done = 1;
-                } else if (cross < n) {
-                    // exact sum just before the crossing element, then one float add
-                    const uint64_t Nprev = Su + (cross > start ? sh.P[cross - 1] : 0);
-                    const double Sprev = (double)Nprev * u;
-                    const double Snew = Sprev + p[base + cross];
-                    sh.S = Snew;
-                    sh.start = cross + 1;
-                    if (mode == 1 && Snew > target) {
-                        sh.found = base + cross;
-                        sh.done = 1;
-                    }
-                } else {
-                    sh.S = (double)(Su + sh.P[n - 1]) * u;
-                    sh.start = n;
+                if (lane == 0) {
+                    sh.S = S;
+                    next_slow = stop;
                 }
             }
             __syncthreads();
-            if (sh.done) break;
+            t = next_slow;
+            if (t >= tile_hi) break;
         }
-        __syncthreads();
+        if (mode == 0 && tid == 0) tile_S[t] = sh.S;
+        walk_tile(p, L, t, mode, target, sh);
         if (sh.done) break;
+        t++;
     }
+    __syncthreads();
     if (tid == 0) {
         if (total) *total = sh.S;
         if (found) *found = sh.found;
@@ -361,15 +529,25 @@ extern "C" int shb_sum(const double *d_x, uint64_t count, double *out, void *str
     return SHB_OK;
 }
 
-// pass 1 -> (total, chunk starts); kept on device in `chunk_S`
-static int seq_total(const double *d_prob, uint64_t count, double *chunk_S, double *total_host, cudaStream_t st)
+// exact walk over all tiles -> (total, exact running sum at every tile start)
+static int seq_total(const double *d_prob, uint64_t count, double *tile_S, double *total_host, cudaStream_t st)
 {
     SHB_TRY(seq_prepare());
-    const uint64_t nch = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
-    Scratch tot;
+    const uint64_t nt = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    Scratch tot, tsum, tstart, recs;
     SHB_TRY(scratch_alloc(tot, sizeof(double), st));
-    seqscan_kernel<<<1, SEQ_THREADS, seq_smem(), st>>>(d_prob, count, 0, nch, 0.0, 0, 0.0, chunk_S,
-                                                         (double *)tot.ptr, nullptr);
+    SHB_TRY(scratch_alloc(tsum, sizeof(double) * nt, st));
+    SHB_TRY(scratch_alloc(tstart, sizeof(double) * nt, st));
+    SHB_TRY(scratch_alloc(recs, sizeof(TileRec) * nt, st));
+    tile_sum_kernel<<<(unsigned)nt, 256, 0, st>>>(d_prob, count, (double *)tsum.ptr);
+    SHB_LAUNCHED();
+    tile_prefix_kernel<<<1, SUM_THREADS, 0, st>>>((const double *)tsum.ptr, nt, (double *)tstart.ptr);
+    SHB_LAUNCHED();
+    tile_rec_kernel<<<(unsigned)nt, 256, 0, st>>>(d_prob, count, (const double *)tstart.ptr, (TileRec *)recs.ptr);
+    SHB_LAUNCHED();
+    seqscan_kernel<<<1, SEQ_THREADS, seq_smem(), st>>>(d_prob, count, 0, nt, 0.0, 0, 0.0,
+                                                         (const TileRec *)recs.ptr, tile_S, (double *)tot.ptr,
+                                                         nullptr);
     SHB_LAUNCHED();
     SHB_TRY_CUDA(cudaGetLastError());
     SHB_TRY_CUDA(cudaMemcpyAsync(total_host, tot.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -389,6 +567,33 @@ extern "C" int shb_cumsum_total(const double *d_prob, uint64_t count, double *to
     return seq_total(d_prob, count, (double *)cs.ptr, total, st);
 }
 
+static int search_from_tiles(const double *d_prob, uint64_t count, const double *d_tile_S, double tot,
+                             double target, uint64_t *index, cudaStream_t st)
+{
+    *index = count;
+    if (!(tot > target)) return SHB_OK;  // no running sum exceeds target -> count
+    const uint64_t nch = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    // tile c ends with running sum tile_S[c+1] (or the total for the last one)
+    std::vector<double> hs(nch);
+    SHB_TRY_CUDA(cudaMemcpyAsync(hs.data(), d_tile_S, sizeof(double) * nch, cudaMemcpyDeviceToHost, st));
+    SHB_TRY_CUDA(cudaStreamSynchronize(st));
+    uint64_t lo = 0, hi = nch - 1;  // first tile whose end value > target
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) / 2;
+        if (hs[mid + 1] > target) hi = mid;
+        else lo = mid + 1;
+    }
+    Scratch fnd;
+    SHB_TRY(scratch_alloc(fnd, sizeof(uint64_t), st));
+    seqscan_kernel<<<1, SEQ_THREADS, seq_smem(), st>>>(d_prob, count, lo, lo + 1, hs[lo], 1, target, nullptr,
+                                                         nullptr, nullptr, (uint64_t *)fnd.ptr);
+    SHB_LAUNCHED();
+    SHB_TRY_CUDA(cudaGetLastError());
+    SHB_TRY_CUDA(cudaMemcpyAsync(index, fnd.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    SHB_TRY_CUDA(cudaStreamSynchronize(st));
+    return SHB_OK;
+}
+
 extern "C" int shb_cumsum_search(const double *d_prob, uint64_t count, double target, uint64_t *index,
                                  void *stream)
 {
@@ -397,28 +602,27 @@ extern "C" int shb_cumsum_search(const double *d_prob, uint64_t count, double ta
     if (count == 0) return SHB_OK;
     cudaStream_t st = as_stream(stream);
     const uint64_t nch = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
-    Scratch cs, fnd;
+    Scratch cs;
     SHB_TRY(scratch_alloc(cs, sizeof(double) * nch, st));
-    SHB_TRY(scratch_alloc(fnd, sizeof(uint64_t), st));
     double tot = 0.0;
     SHB_TRY(seq_total(d_prob, count, (double *)cs.ptr, &tot, st));
-    if (!(tot > target)) return SHB_OK;  // no running sum exceeds target -> count
-    // chunk c ends with running sum chunk_S[c+1] (or the total for the last one)
-    std::vector<double> hs(nch);
-    SHB_TRY_CUDA(cudaMemcpyAsync(hs.data(), cs.ptr, sizeof(double) * nch, cudaMemcpyDeviceToHost, st));
-    SHB_TRY_CUDA(cudaStreamSynchronize(st));
-    uint64_t lo = 0, hi = nch - 1;  // first chunk whose end value > target
-    while (lo < hi) {
-        const uint64_t mid = (lo + hi) / 2;
-        const double end_mid = hs[mid + 1];
-        if (end_mid > target) hi = mid;
-        else lo = mid + 1;
-    }
-    seqscan_kernel<<<1, SEQ_THREADS, seq_smem(), st>>>(d_prob, count, lo, lo + 1, hs[lo], 1, target, nullptr,
-                                                         nullptr, (uint64_t *)fnd.ptr);
-    SHB_LAUNCHED();
-    SHB_TRY_CUDA(cudaGetLastError());
-    SHB_TRY_CUDA(cudaMemcpyAsync(index, fnd.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    SHB_TRY_CUDA(cudaStreamSynchronize(st));
-    return SHB_OK;
+    return search_from_tiles(d_prob, count, (const double *)cs.ptr, tot, target, index, st);
+}
+
+extern "C" int shb_sample_index(const double *d_prob, uint64_t count, double u, uint64_t *index, double *total,
+                                void *stream)
+{
+    if (!index) return set_error(SHB_EINVAL, "null output");
+    *index = count;
+    if (total) *total = 0.0;
+    if (count == 0) return SHB_OK;
+    cudaStream_t st = as_stream(stream);
+    const uint64_t nch = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    Scratch cs;
+    SHB_TRY(scratch_alloc(cs, sizeof(double) * nch, st));
+    double tot = 0.0;
+    SHB_TRY(seq_total(d_prob, count, (double *)cs.ptr, &tot, st));
+    if (total) *total = tot;
+    const double target = u * tot;  // s.uniform() * cum[-1] (qstate.py:143)
+    return search_from_tiles(d_prob, count, (const double *)cs.ptr, tot, target, index, st);
 }

@@ -134,6 +134,26 @@ def dft(amps, length: int, a0: int, stride: int, q: int, c_begin: int, c_count: 
     return out, prob, bsum
 
 
+def dft_uniform(amp: complex, length: int, a0: int, stride: int, q: int, c_begin: int, c_count: int,
+                tiles: int = 1, scale: float | None = None, precision: str = "fp64",
+                want_prob: bool = True):
+    """Direct DFT of a uniform comb (all `length` amplitudes equal `amp`)."""
+    t = _t()
+    prec = PRECISIONS[precision]
+    scale = 1.0 / math.sqrt(q) if scale is None else scale
+    out = t.empty(2 * max(c_count, 1), dtype=t.float64, device="cuda")
+    prob = t.empty(max(c_count, 1), dtype=t.float64, device="cuda") if want_prob else None
+    nb = int(nat.load().shb_dft_num_blocks(c_count, prec))
+    bsum = t.empty(max(nb, 1), dtype=t.float64, device="cuda") if want_prob else None
+    nat.check(nat.load().shb_dft_uniform(float(amp.real), float(amp.imag), length, a0, stride, q, c_begin,
+                                         c_count, tiles, scale, prec, _vp(out), _vp(prob), _vp(bsum),
+                                         _stream()), "dft_uniform")
+    out = out[: 2 * c_count]
+    if want_prob:
+        prob, bsum = prob[:c_count], bsum[:nb]
+    return out, prob, bsum
+
+
 def probabilities(state):
     t = _t()
     n = state.numel() // 2
@@ -159,6 +179,15 @@ def cumsum_search(p, target: float) -> int:
     nat.check(nat.load().shb_cumsum_search(_vp(p), p.numel(), float(target), ctypes.byref(out), _stream()),
               "cumsum_search")
     return int(out.value)
+
+
+def sample_index(p, u: float) -> tuple[int, float]:
+    """searchsorted(cumsum(p), u * cumsum(p)[-1], "right") exactly, and cumsum(p)[-1]."""
+    out = ctypes.c_uint64(0)
+    tot = ctypes.c_double(0.0)
+    nat.check(nat.load().shb_sample_index(_vp(p), p.numel(), float(u), ctypes.byref(out), ctypes.byref(tot),
+                                          _stream()), "sample_index")
+    return int(out.value), float(tot.value)
 
 
 # --------------------------------------------------------------- array types
@@ -258,6 +287,11 @@ class CollapsedAmplitudes(DeviceVector):
         if self.m:
             out[self.support.cpu().numpy()] = self.amp
         return out
+
+    @property
+    def full_comb(self) -> bool:
+        """Every slot of the progression is occupied (always true after measure_part2)."""
+        return self.m == self.length
 
     def progression_amplitudes(self):
         return fill_progression(self.support, self.m, self.a0, self.stride, self.length, self.amp)

@@ -65,12 +65,14 @@ class DeviceOps:
     def dft(self, amps, length, a0, stride, q, c_begin, c_count, precision):
         return self.dev.dft(amps, length, a0, stride, q, c_begin, c_count, precision=precision)
 
+    def dft_uniform(self, amp, length, a0, stride, q, c_begin, c_count, precision):
+        return self.dev.dft_uniform(amp, length, a0, stride, q, c_begin, c_count, precision=precision)
+
     def dsum(self, x):
         return self.dev.dsum(x)
 
     def sample(self, prob, u):
-        total = self.dev.cumsum_total(prob)
-        return self.dev.cumsum_search(prob, u * total)
+        return self.dev.sample_index(prob, u)[0]
 
     def empty(self, n, dtype):
         return self.torch.empty(n, dtype=dtype, device=self.device)
@@ -151,7 +153,9 @@ def sharded_attempt(n: int, x: int, q: int, sampler: qstate.Sampler, *, rank: in
     M = int(sup.numel())
     amp = qstate.collapsed_amplitude(a_unif, w0, M)
     a0, stride, length = ops.progression(sup)
-    amps = ops.fill_progression(sup, M, a0, stride, length, amp)
+    # the collapsed support is a full comb: uniform-comb kernel;
+    # anything else goes through the generic amplitude stream
+    amps = None if M == length else ops.fill_progression(sup, M, a0, stride, length, amp)
     del res
     t0 = tick("measure2", t0)
 
@@ -161,7 +165,10 @@ def sharded_attempt(n: int, x: int, q: int, sampler: qstate.Sampler, *, rank: in
     if time_dft and torch.cuda.is_available():
         ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         ev[0].record()
-    out, prob, bsum = ops.dft(amps, length, a0, stride, q, c_lo, c_hi - c_lo, precision)
+    if amps is None:
+        out, prob, bsum = ops.dft_uniform(amp, length, a0, stride, q, c_lo, c_hi - c_lo, precision)
+    else:
+        out, prob, bsum = ops.dft(amps, length, a0, stride, q, c_lo, c_hi - c_lo, precision)
     if ev is not None:
         ev[1].record()
     t0 = tick("qft", t0)

@@ -102,17 +102,22 @@ def build_twiddles(q: int, max_width: int = 24) -> TwiddleTable:
 # ------------------------------------------------------------- device engine
 
 def _support_of(state, q: int):
-    """(amps device tensor, length, a0, stride, host_input) for any state form."""
+    """(amps, length, a0, stride, host_input) for any state form.
+
+    amps is a device tensor, or a Python complex when every progression slot
+    holds the same amplitude (the uniform-comb kernel is selected from the data).
+    """
     t = nat.require_cuda()
     if isinstance(state, dev.CollapsedAmplitudes):
         if state.q != q:
             raise ValueError(f"state length {(state.q,)} does not match q={q}")
+        if state.full_comb:
+            return state.amp, state.length, state.a0, state.stride, False
         return state.progression_amplitudes(), state.length, state.a0, state.stride, False
     if isinstance(state, dev.UniformAmplitudes):
         if state.q != q:
             raise ValueError(f"state length {(state.q,)} does not match q={q}")
-        amps = dev.fill_progression(None, q, 0, 1, q, complex(state.value))
-        return amps, q, 0, 1, False
+        return complex(state.value), q, 0, 1, False
     if isinstance(state, dev.DeviceSpectrum):
         if state.q != q:
             raise ValueError(f"state length {(state.q,)} does not match q={q}")
@@ -131,8 +136,12 @@ def _support_of(state, q: int):
 
 def _run(state, q: int, tiles: int, precision: str):
     amps, length, a0, stride, host = _support_of(state, q)
-    out, prob, bsum = dev.dft(amps, length, a0, stride, q, 0, q, tiles=tiles,
-                              scale=1.0 / math.sqrt(q), precision=precision)
+    if isinstance(amps, complex):
+        out, prob, bsum = dev.dft_uniform(amps, length, a0, stride, q, 0, q, tiles=tiles,
+                                          scale=1.0 / math.sqrt(q), precision=precision)
+    else:
+        out, prob, bsum = dev.dft(amps, length, a0, stride, q, 0, q, tiles=tiles,
+                                  scale=1.0 / math.sqrt(q), precision=precision)
     spec = dev.DeviceSpectrum(q, out, prob, bsum)
     return spec.numpy() if host else spec
 

@@ -190,9 +190,7 @@ def sample_part1(reg: CompositeRegister, s: Sampler) -> int:
     """Born-rule read of part 1 (qstate.py:138-144), exact sequential CDF on the GPU."""
     _require_normalized(reg)
     p = _device_probabilities(reg)
-    total = dev.cumsum_total(p)
-    target = s.uniform() * total
-    m = dev.cumsum_search(p, target)
+    m, _ = dev.sample_index(p, s.uniform())  # target = u * cum[-1], as qstate.py:143
     return min(m, reg.q - 1)
 
 

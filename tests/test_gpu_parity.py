@@ -148,13 +148,20 @@ def test_dft_vs_reference_rows(golden_dir, tag):
     if q <= (1 << 16):
         out, prob, _ = dev.dft(amps, M, c0, r, q, 0, q)
         _check_spectrum(_rows(out, rows), d["V"])
-        # fused probabilities are |V|^2 as numpy computes them
+        # fused probabilities are hypot(re, im)^2 (qstate.py:141); CUDA's hypot
+        # is not glibc's, so equal to within a few ulp rather than bitwise
         p_host = prob.cpu().numpy()
-        assert np.array_equal(p_host, np.abs(out.cpu().numpy().view(np.complex128)) ** 2)
+        p_np = np.abs(out.cpu().numpy().view(np.complex128)) ** 2
+        assert np.all(np.abs(p_host - p_np) <= 4 * np.spacing(p_np))
+        # the uniform-comb kernel (selected for collapsed registers) agrees too
+        ou, pu, _ = dev.dft_uniform(_amp(info), M, c0, r, q, 0, q)
+        _check_spectrum(_rows(ou, rows), d["V"])
     else:
         for c in rows[:64]:
             out, _, _ = dev.dft(amps, M, c0, r, q, int(c), 1)
             _check_spectrum(out.cpu().numpy().view(np.complex128), d["V"][rows == c])
+            ou, _, _ = dev.dft_uniform(_amp(info), M, c0, r, q, int(c), 1)
+            _check_spectrum(ou.cpu().numpy().view(np.complex128), d["V"][rows == c])
 
 
 def test_dft_full_vs_closed_form_2_24(golden_dir):
@@ -162,8 +169,7 @@ def test_dft_full_vs_closed_form_2_24(golden_dir):
     info = json.loads(str(d["info"]))
     q, M, c0, r = int(d["q"]), info["M"], info["c0"], info["r"]
     sup = torch.arange(M, dtype=torch.int64, device="cuda") * r + c0
-    amps = dev.fill_progression(sup, M, c0, r, M, _amp(info))
-    out, prob, bsum = dev.dft(amps, M, c0, r, q, 0, q)
+    out, prob, bsum = dev.dft_uniform(_amp(info), M, c0, r, q, 0, q)
     p = prob.cpu().numpy()
     rows = np.random.default_rng(5).choice(q, 20000, replace=False)
     cf = oracle.comb_probabilities(q, r, c0, M, rows)
@@ -181,8 +187,10 @@ def test_fp32_fast_path(golden_dir):
     amps = dev.fill_progression(sup, M, c0, r, M, _amp(info))
     _, p32, _ = dev.dft(amps, M, c0, r, q, 0, q, precision="fp32")
     _, p64, _ = dev.dft(amps, M, c0, r, q, 0, q, precision="fp64")
-    p32, p64 = p32.cpu().numpy(), p64.cpu().numpy()
+    _, pu32, _ = dev.dft_uniform(_amp(info), M, c0, r, q, 0, q, precision="fp32")
+    p32, p64, pu32 = p32.cpu().numpy(), p64.cpu().numpy(), pu32.cpu().numpy()
     assert np.max(np.abs(p32 - p64)) / p64.max() <= 1e-4
+    assert np.max(np.abs(pu32 - p64)) / p64.max() <= 1e-4
 
 
 def test_random_states_dense_tiled(golden_dir):
@@ -227,11 +235,12 @@ def test_dft_sharded_rows_bitwise_identical():
     q, c0, r, M = 1 << 18, 11, 12, ((1 << 18) - 1 - 11) // 12 + 1
     sup = torch.arange(M, dtype=torch.int64, device="cuda") * r + c0
     amps = dev.fill_progression(sup, M, c0, r, M, complex(1 / math.sqrt(M)))
-    full, _, _ = dev.dft(amps, M, c0, r, q, 0, q)
-    full = full.cpu().numpy()
-    for g in (2, 4, 8):
-        parts = [dev.dft(amps, M, c0, r, q, s * q // g, q // g)[0].cpu().numpy() for s in range(g)]
-        assert np.array_equal(np.concatenate(parts).view(np.uint64), full.view(np.uint64))
+    for fn in (lambda lo, cnt: dev.dft(amps, M, c0, r, q, lo, cnt)[0],
+               lambda lo, cnt: dev.dft_uniform(complex(1 / math.sqrt(M)), M, c0, r, q, lo, cnt)[0]):
+        full = fn(0, q).cpu().numpy()
+        for g in (2, 4, 8):
+            parts = [fn(s * q // g, q // g).cpu().numpy() for s in range(g)]
+            assert np.array_equal(np.concatenate(parts).view(np.uint64), full.view(np.uint64))
 
 
 def test_host_abi_dropins(golden_dir):
@@ -262,9 +271,12 @@ def _adversarial_probs(rng, n):
         np.full(n, 2.0 ** -20),
         (rng.integers(0, 4, n) * 2.0 ** -30),
         np.exp(rng.normal(-30, 12, n)),
-        np.concatenate([[1e-300, 5e-324], rng.random(n - 2) * 1e-9]),
+        np.concatenate([[1e-300, 5e-324], rng.random(n - 2) * 1e-9])[:n],
+        # odd multiples of 2^-54: every add in [0.5, 1) is an exact round-half-even tie
+        (2 * rng.integers(0, 1 << 10, n) + 1) * 2.0 ** -54,
     ]
-    return [np.ascontiguousarray(k / k.sum() if k.sum() > 0 else k) for k in kinds]
+    out = [np.ascontiguousarray(k / k.sum() if k.sum() > 0 else k) for k in kinds[:-1]]
+    return out + [np.ascontiguousarray(kinds[-1])]
 
 
 @pytest.mark.parametrize("n", [1, 7, 8192, 8193, 100003, 1 << 20])
@@ -283,6 +295,10 @@ def test_exact_cumsum_emulation(n):
         for i in rng.integers(0, n, 5):
             want = int(np.searchsorted(cum, cum[i], side="right"))
             assert dev.cumsum_search(pd, float(cum[i])) == want
+        # the fused Born-rule read used by sample_part1
+        u = float(rng.random())
+        m, tot = dev.sample_index(pd, u)
+        assert tot == cum[-1] and m == int(np.searchsorted(cum, u * cum[-1], side="right"))
 
 
 def test_sample_part1_vs_reference(golden_dir):
