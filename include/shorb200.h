@@ -87,6 +87,12 @@ int shb_state_progression(const double *d_state, uint64_t q, uint64_t *a0,
 int shb_gather_progression(const double *d_state, uint64_t a0, uint64_t stride,
                            uint64_t length, double *d_amps, void *stream);
 
+/* *uniform = 1 if all `length` complex128 amplitudes are bitwise equal, and
+ * the common value in (*amp_re, *amp_im): selects the uniform-comb kernel. */
+int shb_progression_is_uniform(const double *d_amps, uint64_t length,
+                               int *uniform, double *amp_re, double *amp_im,
+                               void *stream);
+
 /* d_amps[j] = amp for j < length where the support index a0 + j*stride is in
  * d_support[0..m), 0 otherwise (collapsed register -> progression amplitudes). */
 int shb_fill_progression(const uint64_t *d_support, uint64_t m, uint64_t a0,

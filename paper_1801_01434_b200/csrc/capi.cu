@@ -160,16 +160,18 @@ struct PairwiseConst {
 // 4 CTAs x 256 threads per SM.  The roofline denominator of the QFT kernel.
 __global__ void __launch_bounds__(256) fp64_probe_kernel(double *out, int iters, double a, double b)
 {
-    double x[8];
+    double x[16];
 #pragma unroll
-    for (int i = 0; i < 8; i++) x[i] = threadIdx.x * 1e-3 + i;
-    for (int it = 0; it < iters; it++) {
+    for (int i = 0; i < 16; i++) x[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters; it += 4) {
 #pragma unroll
-        for (int i = 0; i < 8; i++) x[i] = fma(x[i], a, b);
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int i = 0; i < 16; i++) x[i] = fma(x[i], a, b);
     }
     double s = 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++) s += x[i];
+    for (int i = 0; i < 16; i++) s += x[i];
     if (s == 1234.5) out[0] = s;  // keep the chains alive
 }
 
@@ -227,7 +229,7 @@ int shb_fp64_peak(double seconds, double *tflops, void *stream)
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    const double flops = 2.0 * 8.0 * (double)iters * 256.0 * grid * reps;
+    const double flops = 2.0 * 16.0 * (double)iters * 256.0 * grid * reps;
     *tflops = flops / (ms * 1e-3) / 1e12;
     return SHB_OK;
 }
@@ -266,8 +268,17 @@ static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t i
         if (len) SHB_TRY(shb_gather_progression((const double *)d_state.ptr, a0, stride, len,
                                                 (double *)d_amps.ptr, st));
         SHB_TRY(scratch_alloc(d_out, c_count * 16, st));
-        rc = shb_dft((const double *)d_amps.ptr, len, a0 + index_base, stride, q, c_begin, c_count,
-                     tiles, scale, precision, (double *)d_out.ptr, nullptr, nullptr, st);
+        // data-selected kernel: a uniform comb (e.g. a collapsed register) takes the
+        // constant-operand path, anything else the TMA-staged amplitude stream
+        int uni = 0;
+        double ur = 0.0, ui = 0.0;
+        if (len) SHB_TRY(shb_progression_is_uniform((const double *)d_amps.ptr, len, &uni, &ur, &ui, st));
+        if (uni)
+            rc = shb_dft_uniform(ur, ui, len, a0 + index_base, stride, q, c_begin, c_count, tiles, scale,
+                                 precision, (double *)d_out.ptr, nullptr, nullptr, st);
+        else
+            rc = shb_dft((const double *)d_amps.ptr, len, a0 + index_base, stride, q, c_begin, c_count,
+                         tiles, scale, precision, (double *)d_out.ptr, nullptr, nullptr, st);
         if (rc != SHB_OK) return rc;
         SHB_TRY_CUDA(cudaMemcpyAsync(out_host, d_out.ptr, c_count * 16, cudaMemcpyDeviceToHost, st));
     }

@@ -228,6 +228,21 @@ __global__ void scatter_support_kernel(const uint64_t *__restrict__ s, uint64_t 
         amps[(s[i] - a0) / stride] = v;
 }
 
+// all amplitudes of a progression equal to the first one?
+__global__ void uniform_check_kernel(const double2 *__restrict__ amps, uint64_t len, unsigned int *__restrict__ diff)
+{
+    const double2 a0 = amps[0];
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    bool d = false;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += step) {
+        const double2 v = amps[j];
+        // bitwise comparison: -0.0 and +0.0 or NaN payloads are not "equal"
+        d |= (__double_as_longlong(v.x) != __double_as_longlong(a0.x)) ||
+             (__double_as_longlong(v.y) != __double_as_longlong(a0.y));
+    }
+    if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(diff, 1u);
+}
+
 static unsigned grid_for(uint64_t n, int threads, int per_sm)
 {
     uint64_t b = (n + threads - 1) / threads;
@@ -325,6 +340,31 @@ extern "C" int shb_gather_progression(const double *d_state, uint64_t a0, uint64
                                                                 (double2 *)d_amps);
     SHB_LAUNCHED();
     SHB_TRY_CUDA(cudaGetLastError());
+    return SHB_OK;
+}
+
+extern "C" int shb_progression_is_uniform(const double *d_amps, uint64_t length, int *uniform, double *amp_re,
+                                          double *amp_im, void *stream)
+{
+    if (!uniform) return set_error(SHB_EINVAL, "null output");
+    *uniform = 0;
+    if (length == 0) return SHB_OK;
+    cudaStream_t st = as_stream(stream);
+    Scratch diff;
+    SHB_TRY(scratch_alloc(diff, sizeof(unsigned int), st));
+    SHB_TRY_CUDA(cudaMemsetAsync(diff.ptr, 0, sizeof(unsigned int), st));
+    uniform_check_kernel<<<grid_for(length, 256, 8), 256, 0, st>>>((const double2 *)d_amps, length,
+                                                                  (unsigned int *)diff.ptr);
+    SHB_LAUNCHED();
+    SHB_TRY_CUDA(cudaGetLastError());
+    unsigned int h = 1;
+    double a[2] = {0.0, 0.0};
+    SHB_TRY_CUDA(cudaMemcpyAsync(&h, diff.ptr, sizeof h, cudaMemcpyDeviceToHost, st));
+    SHB_TRY_CUDA(cudaMemcpyAsync(a, d_amps, sizeof a, cudaMemcpyDeviceToHost, st));
+    SHB_TRY_CUDA(cudaStreamSynchronize(st));
+    *uniform = h ? 0 : 1;
+    if (amp_re) *amp_re = a[0];
+    if (amp_im) *amp_im = a[1];
     return SHB_OK;
 }
 

@@ -103,6 +103,17 @@ def gather_progression(state, a0: int, stride: int, length: int):
     return amps
 
 
+def progression_uniform(amps, length: int):
+    """The common amplitude if all progression amplitudes are equal, else None."""
+    if length == 0:
+        return None
+    u = ctypes.c_int(0)
+    re, im = ctypes.c_double(), ctypes.c_double()
+    nat.check(nat.load().shb_progression_is_uniform(_vp(amps), length, ctypes.byref(u), ctypes.byref(re),
+                                                    ctypes.byref(im), _stream()), "progression_is_uniform")
+    return complex(re.value, im.value) if u.value else None
+
+
 def fill_progression(support, m: int, a0: int, stride: int, length: int, amp: complex):
     t = _t()
     amps = t.empty(2 * max(length, 1), dtype=t.float64, device="cuda")

@@ -131,6 +131,9 @@ def _support_of(state, q: int):
         host = True
     a0, stride, length = dev.state_progression(data)
     amps = dev.gather_progression(data, a0, stride, length) if length else None
+    uni = dev.progression_uniform(amps, length) if length else None
+    if uni is not None:
+        return uni, length, a0, stride, host
     return amps, length, a0, stride, host
 
 

@@ -152,7 +152,7 @@ def test_dft_vs_reference_rows(golden_dir, tag):
         # is not glibc's, so equal to within a few ulp rather than bitwise
         p_host = prob.cpu().numpy()
         p_np = np.abs(out.cpu().numpy().view(np.complex128)) ** 2
-        assert np.all(np.abs(p_host - p_np) <= 4 * np.spacing(p_np))
+        assert np.max(np.abs(p_host - p_np) / np.spacing(p_np)) <= 8
         # the uniform-comb kernel (selected for collapsed registers) agrees too
         ou, pu, _ = dev.dft_uniform(_amp(info), M, c0, r, q, 0, q)
         _check_spectrum(_rows(ou, rows), d["V"])
