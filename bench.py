@@ -291,15 +291,24 @@ def run_b200(args):
     peak_tf = ptf.value
     dft_s = statistics.mean(dft_ms) / 1000.0
     achieved_tf = 8.0 * rec.phase_terms / dft_s / 1e12
+    # DRAM bytes per DFT launch from the committed ncu --set full capture, only
+    # when that capture was taken at this very configuration
     prof = ROOT / "profiles" / "dft_traffic.json"
-    traffic = None
+    traffic, traffic_note = None, "no ncu --set full capture at this config"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("bytes_per_launch_at_bench_config")
+            tj = json.loads(prof.read_text())
+            if tj.get("config") == f"n={args.n} q=2^{q.bit_length() - 1} M={rec.M}":
+                traffic = tj["dram_bytes_per_launch"] / world
+                traffic_note = f"ncu capture {tj.get('source', '')}".strip()
+            else:
+                traffic_note = (f"ncu capture at {tj.get('config')} measured {tj['dram_bytes_per_launch'] / 1e6:.1f} MB "
+                                f"vs {tj['algorithmic_bytes_per_launch'] / 1e6:.1f} MB algorithmic (24 B/output)")
         except Exception:
-            traffic = None
+            pass
     roof = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-            "frac": achieved_tf / peak_tf, "traffic": traffic,
+            "frac": achieved_tf / peak_tf, "traffic": traffic, "traffic_note": traffic_note,
+            "traffic_unit": "bytes/launch", "algorithmic_bytes_per_launch": 24 * (q // world),
             "peak_source": "measured on this GPU by shb_fp64_peak (independent DFMA chains); "
                            "MEASURED_PEAKS.json has no FP64 figure; nominal 37.2 TF at 1965 MHz",
             "kernel": "shb::dft_kernel<double>", "dft_ms_per_launch": dft_s * 1000.0,

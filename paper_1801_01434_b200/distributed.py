@@ -184,15 +184,11 @@ def sharded_attempt(n: int, x: int, q: int, sampler: qstate.Sampler, *, rank: in
     # (4) probability shards -> rank 0 -> exact sequential CDF -> m to all ranks
     u = sampler.uniform()
     if world > 1:
-        parts = [torch.empty(shard(q, g, world)[1] - shard(q, g, world)[0], dtype=prob.dtype,
-                             device=prob.device) for g in range(world)]
-        dist.all_gather(parts, prob.contiguous(), group=group)
+        full, _ = _all_gather_var(prob.contiguous(), world, group, torch)  # shards in c order
         mt = torch.zeros(1, dtype=torch.int64, device=prob.device)
         if rank == 0:
-            full = torch.cat(parts)
             mt[0] = ops.sample(full, u)
-            del full
-        del parts
+        del full
         dist.broadcast(mt, src=0, group=group)
         m = int(mt.item())
     else:

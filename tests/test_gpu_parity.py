@@ -271,7 +271,7 @@ def _adversarial_probs(rng, n):
         np.full(n, 2.0 ** -20),
         (rng.integers(0, 4, n) * 2.0 ** -30),
         np.exp(rng.normal(-30, 12, n)),
-        np.concatenate([[1e-300, 5e-324], rng.random(n - 2) * 1e-9])[:n],
+        np.concatenate([[1e-300, 5e-324], rng.random(max(n - 2, 0)) * 1e-9])[:n],
         # odd multiples of 2^-54: every add in [0.5, 1) is an exact round-half-even tie
         (2 * rng.integers(0, 1 << 10, n) + 1) * 2.0 ** -54,
     ]
