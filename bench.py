@@ -331,14 +331,11 @@ def run_b200(args):
         "phase_ms_last_step": {k: v * 1000 for k, v in rec.phase_times.items()},
     }
 
-    # e2e: the reference-facing C-ABI drop-in with HOST buffers (dense_dft over a
-    # pinned complex128[q] state, H2D + DFT + D2H inside the timed region)
-    if not args.no_e2e and world == 1:
-        line["e2e"] = e2e_host(args, q, x, lib, torch, nat)
-    elif not args.no_e2e:
-        line["e2e"] = {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
-                       "path": "sharded pipeline from (n, seed); host-buffer e2e measured at N=1 only"}
-
+    # e2e: the reference-facing C-ABI drop-in with HOST buffers (H2D + DFT + D2H
+    # inside the timed region).  N=1: shb_dense_dft_host (qft.dense_dft); N>1:
+    # every rank runs the _kernels.partial_row_sums seam on its row shard.
+    if not args.no_e2e:
+        line["e2e"] = e2e_host(args, q, x, lib, torch, nat, rank, world)
     if not args.no_factoring:
         from paper_1801_01434_b200 import qft
         barrier()
@@ -374,17 +371,31 @@ def ctypes_double():
     return ctypes.c_double(0.0)
 
 
-def e2e_host(args, q, x, lib, torch, nat):
+def e2e_host(args, q, x, lib, torch, nat, rank=0, world=1):
     import ctypes
     import numpy as np
     k, c0, r, M, amp = comb_of(args.n, x, q, args.seed)
+    c_lo, c_hi = q * rank // world, q * (rank + 1) // world
+    need = 16 * q + 16 * (c_hi - c_lo)
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:  # pragma: no cover
+        avail = None
+    ok = avail is None or world * need < 0.8 * avail
+    if world > 1:
+        flag = torch.tensor([1 if ok else 0], device="cuda")
+        torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+        ok = bool(flag.item())
+    if not ok:
+        return {"value": None, "unit": UNIT, "h2d_bytes_per_step": 16 * q, "d2h_bytes_per_step": 16 * q,
+                "reason": f"host RAM: {world} ranks x {need / 2**30:.0f} GiB pinned exceeds 80% of available"}
     st = torch.empty(2 * q, dtype=torch.float64, pin_memory=True)
-    out = torch.empty(2 * q, dtype=torch.float64, pin_memory=True)
+    out = torch.empty(2 * (c_hi - c_lo), dtype=torch.float64, pin_memory=True)
     stn = st.numpy().view(np.complex128)
     stn[:] = 0
     stn[c0::r] = amp
     prec = 0 if args.precision == "fp64" else 1
-    steps = 1
     # warm the path once at a small size (allocator pools, schedule upload)
     small = np.zeros(1024, dtype=np.complex128)
     small[3::7] = 0.1
@@ -392,18 +403,28 @@ def e2e_host(args, q, x, lib, torch, nat):
     nat.check(lib.shb_dense_dft_host(ctypes.c_void_p(small.ctypes.data), 1024, 1, prec,
                                      ctypes.c_void_p(so.ctypes.data)))
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
-    for _ in range(steps):
+    if world == 1:
         nat.check(lib.shb_dense_dft_host(ctypes.c_void_p(st.data_ptr()), q, 1, prec,
                                          ctypes.c_void_p(out.data_ptr())), "dense_dft_host")
+        api = "shb_dense_dft_host (C ABI of qft.dense_dft, pinned host buffers)"
+    else:
+        nat.check(lib.shb_partial_row_sums_host(ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.data_ptr()),
+                                                None, q, c_lo, c_hi, 0, q), "partial_row_sums_host")
+        api = "shb_partial_row_sums_host (C ABI of _kernels.partial_row_sums), row shard per rank"
     el = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([el], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        el = float(t.item())
     o = out.numpy().view(np.complex128)
-    peak = o[(q // r) * 0]
+    v0 = o[0] if rank == 0 else complex(0)
     del st, out
-    return {"value": q * M * steps / el, "unit": UNIT, "h2d_bytes_per_step": 16 * q,
-            "d2h_bytes_per_step": 16 * q, "steps": steps, "seconds": el,
-            "api": "shb_dense_dft_host (C ABI of qft.dense_dft, pinned host buffers)",
-            "check_V0": [float(peak.real), float(peak.imag)]}
+    return {"value": q * M / el, "unit": UNIT, "h2d_bytes_per_step": 16 * q * world,
+            "d2h_bytes_per_step": 16 * q, "steps": 1, "seconds": el, "api": api,
+            "check_V0": [float(v0.real), float(v0.imag)]}
 
 
 def main():

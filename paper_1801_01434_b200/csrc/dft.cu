@@ -85,7 +85,7 @@ struct DftArgs {
     double *block_sums;
 };
 
-template <typename R, bool UNIF>
+template <typename R, bool UNIF, bool TILED>
 __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
 {
     constexpr int K = Prec<R>::K;
@@ -99,9 +99,10 @@ __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
     const uint64_t cblk = (uint64_t)blockIdx.x * DFT_THREADS * K;
 
     // per-output state: step rotation (cos, sin) of phi = 2 pi stride c / q,
-    // Horner acc (h), tile partial (t), running total (v)
+    // Horner acc (h), tile partial (t, only when tiles > 1), running total (v)
+    constexpr int KT = TILED ? K : 1;
     R wr[K], wi[K], hr[K], hi[K];
-    double tr[K], ti[K], vr[K], vi[K];
+    double tr[KT], ti[KT], vr[K], vi[K];
     uint64_t cval[K];
 #pragma unroll
     for (int i = 0; i < K; i++) {
@@ -111,8 +112,10 @@ __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
         wr[i] = (R)co;
         wi[i] = (R)si;
         hr[i] = hi[i] = (R)0;
-        tr[i] = ti[i] = vr[i] = vi[i] = 0.0;
+        vr[i] = vi[i] = 0.0;
     }
+#pragma unroll
+    for (int i = 0; i < KT; i++) tr[i] = ti[i] = 0.0;
 
     if (!UNIF) {
         if (tid == 0) {
@@ -180,17 +183,22 @@ __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
                 double sc, ss;
                 phase((a_last * cval[i]) & qmask, q, p.two_over_q, sc, ss);
                 const double xr = (double)hr[i], xi = (double)hi[i];
-                tr[i] = fma(sc, xr, fma(-ss, xi, tr[i]));
-                ti[i] = fma(sc, xi, fma(ss, xr, ti[i]));
+                if (TILED) {
+                    tr[i % KT] = fma(sc, xr, fma(-ss, xi, tr[i % KT]));
+                    ti[i % KT] = fma(sc, xi, fma(ss, xr, ti[i % KT]));
+                } else {
+                    vr[i] = fma(sc, xr, fma(-ss, xi, vr[i]));
+                    vi[i] = fma(sc, xi, fma(ss, xr, vi[i]));
+                }
                 hr[i] = hi[i] = (R)0;
             }
         }
-        if (d.flags & CH_TILE_END) {
+        if (TILED && (d.flags & CH_TILE_END)) {
 #pragma unroll
             for (int i = 0; i < K; i++) {
-                vr[i] += tr[i];
-                vi[i] += ti[i];
-                tr[i] = ti[i] = 0.0;
+                vr[i] += tr[i % KT];
+                vi[i] += ti[i % KT];
+                tr[i % KT] = ti[i % KT] = 0.0;
             }
         }
         if (!UNIF) {
@@ -228,8 +236,8 @@ __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
     }
 }
 
-template <typename R, bool UNIF>
-static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t st)
+template <typename R, bool UNIF, bool TILED>
+static int launch_dft_t(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t st)
 {
     constexpr int K = Prec<R>::K;
     const uint64_t SEG = Prec<R>::SEG;
@@ -268,17 +276,25 @@ static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t s
     const size_t smem = UNIF ? 0 : (size_t)DFT_STAGES * DFT_CHUNK * sizeof(double2);
     static bool attr_done = false;
     if (!attr_done && smem) {
-        SHB_TRY_CUDA(cudaFuncSetAttribute(dft_kernel<R, UNIF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SHB_TRY_CUDA(cudaFuncSetAttribute(dft_kernel<R, UNIF, TILED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
         attr_done = true;
     }
     const uint64_t per_blk = (uint64_t)DFT_THREADS * K;
     const uint64_t nblk = (a.c_count + per_blk - 1) / per_blk;
     if (nblk > 0x7FFFFFFFull) return set_error(SHB_EINVAL, "too many outputs for one launch");
-    dft_kernel<R, UNIF><<<(unsigned)nblk, DFT_THREADS, smem, st>>>(a);
+    dft_kernel<R, UNIF, TILED><<<(unsigned)nblk, DFT_THREADS, smem, st>>>(a);
     SHB_LAUNCHED();
     SHB_TRY_CUDA(cudaGetLastError());
     return SHB_OK;
+}
+
+template <typename R, bool UNIF>
+static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t st)
+{
+    // tile partials only exist for the reference's tiled engine (qft.py:290-317)
+    return tiles > 1 ? launch_dft_t<R, UNIF, true>(a, length, tiles, st)
+                     : launch_dft_t<R, UNIF, false>(a, length, tiles, st);
 }
 
 static int validate(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin,

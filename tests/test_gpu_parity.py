@@ -346,3 +346,26 @@ def test_pipeline_q2_24_properties():
     assert abs(qstate.l2_norm(qstate.CompositeRegister(1 << 24, spec, None)) - 1.0) < 1e-9
     m = qstate.sample_part1(qstate.CompositeRegister(1 << 24, spec, None), s)
     assert m == 578525
+
+
+def test_full_spectrum_q2_30_vs_cufft():
+    """Whole q = 2^30 spectrum against an independent oracle (test-only):
+    V_k = (1/sqrt q) sum_j e^{+2 pi i jk/q} V_j = sqrt(q) * ifft(V)[k] (cuFFT).
+    A sparse comb (M = 1031) keeps the direct DFT at ~1e12 phase terms."""
+    q = 1 << 30
+    c0, r, M = 12345, 1_000_003, 1031
+    amp = complex(1.0 / math.sqrt(M))
+    out, prob, bsum = dev.dft_uniform(amp, M, c0, r, q, 0, q)
+    state = torch.zeros(q, dtype=torch.complex128, device="cuda")
+    state[c0: c0 + r * M: r] = amp
+    ref = torch.fft.ifft(state) * math.sqrt(q)
+    del state
+    got = out.view(torch.complex128)
+    assert float((got - ref).abs().max()) < 1e-12
+    pr = ref.abs() ** 2
+    assert float((prob - pr).abs().max() / pr.max()) < 1e-9
+    assert abs(dev.dsum(bsum) - 1.0) < 1e-9
+    # generic (TMA-staged) kernel on the same comb, output shard only
+    amps = dev.fill_progression(None, M, c0, r, M, amp)
+    part, _, _ = dev.dft(amps, M, c0, r, q, q // 2, 1 << 20)
+    assert float((part.view(torch.complex128) - ref[q // 2: q // 2 + (1 << 20)]).abs().max()) < 1e-12
