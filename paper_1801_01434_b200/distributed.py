@@ -201,3 +201,39 @@ def sharded_attempt(n: int, x: int, q: int, sampler: qstate.Sampler, *, rank: in
     if keep_spectrum:
         rec.spectrum = (out, prob)
     return rec
+
+
+def dump_spectrum_sharded(out, q: int, path, *, rank: int = 0, world: int = 1, group=None,
+                          chunk_elems: int = 1 << 22) -> None:
+    """QREG dump (qstate.dump_state format, qstate.py:151-160) of a c-sharded
+    spectrum: rank 0 writes the 16-byte header and sizes the file, then every
+    rank writes its own slice [g q/G, (g+1) q/G) at its byte offset in 64 MiB
+    pieces.  `out` is this rank's float64 [2 * shard] (interleaved re, im)
+    tensor; the file equals qstate.dump_state of the gathered spectrum."""
+    import os
+
+    import numpy as np
+
+    from . import qstate as qs
+    w = q.bit_length() - 1
+    if rank == 0:
+        with open(path, "wb") as fh:
+            fh.write(qs._DUMP_HEADER.pack(qs._DUMP_MAGIC, qs._DUMP_VERSION, w, 0))
+            fh.truncate(qs._DUMP_HEADER.size + 16 * q)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier(group=group)
+    c_lo, c_hi = shard(q, rank, world)
+    if out.numel() != 2 * (c_hi - c_lo):
+        raise ValueError("spectrum shard does not match this rank's output slice")
+    fd = os.open(path, os.O_WRONLY)
+    try:
+        for lo in range(0, c_hi - c_lo, chunk_elems):
+            hi = min(c_hi - c_lo, lo + chunk_elems)
+            buf = out[2 * lo: 2 * hi].cpu().numpy().astype("<f8", copy=False).tobytes()
+            os.pwrite(fd, buf, qs._DUMP_HEADER.size + 16 * (c_lo + lo))
+    finally:
+        os.close(fd)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier(group=group)

@@ -84,12 +84,18 @@ def _attempts(n, seed, q, rank, world, group, count):
     return out
 
 
-def _worker(rank, world, port, cases, ret):
+def _worker(rank, world, port, cases, ret, dump_path=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         res = [_attempts(n, seed, q, rank, world, None, count) for n, seed, q, count in cases]
         ret[rank] = res
+        if dump_path:
+            q = 256
+            lo, hi = D.shard(q, rank, world)
+            full = (np.arange(q) * (1 + 0.5j)).astype(np.complex128)
+            D.dump_spectrum_sharded(torch.from_numpy(full[lo:hi].view(np.float64).copy()), q, dump_path,
+                                    rank=rank, world=world)
     finally:
         dist.destroy_process_group()
 
@@ -109,12 +115,13 @@ def single():
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_attempts_match_single_rank(world, single):
+def test_sharded_attempts_match_single_rank(world, single, tmp_path):
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     ret = mgr.dict()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, ret)) for r in range(world)]
+    dump = str(tmp_path / "spec.qreg")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, ret, dump)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -129,6 +136,9 @@ def test_sharded_attempts_match_single_rank(world, single):
                 if "norm2" in g:
                     assert abs(g["norm2"] - 1.0) < 1e-12
                     assert g["terms"] * world >= s["terms"] - s["M"] * world
+    # sharded QREG dump == the single-writer dump of the gathered spectrum
+    full = (np.arange(256) * (1 + 0.5j)).astype(np.complex128)
+    assert np.array_equal(qstate.load_state(dump), full)
 
 
 def test_single_rank_matches_reference_traces(single, golden_dir):
