@@ -369,3 +369,15 @@ def test_full_spectrum_q2_30_vs_cufft():
     amps = dev.fill_progression(None, M, c0, r, M, amp)
     part, _, _ = dev.dft(amps, M, c0, r, q, q // 2, 1 << 20)
     assert float((part.view(torch.complex128) - ref[q // 2: q // 2 + (1 << 20)]).abs().max()) < 1e-12
+
+
+def test_cli_factor_and_bench_suite(capsys):
+    from paper_1801_01434_b200 import cli
+    assert cli.main(["factor", "--n", "77", "--kernel", "dense"]) == 0
+    out = json.loads(capsys.readouterr().out)
+    assert out["factors"] == [7, 11] and out["qft_fraction"] > 0
+    # SPEC acceptance 1 (cofactor multisets of Table 3), small suite, two engine names
+    assert cli.main(["bench", "--suite", "table3-small", "--engines", "dense,fft", "--format", "csv"]) == 0
+    lines = capsys.readouterr().out.strip().splitlines()
+    cof = {(ln.split(",")[0], ln.split(",")[2]): ln.split(",")[1] for ln in lines[1:]}
+    assert cof[("77", "dense")] == "7x11" and cof[("231", "fft")] == "3x7x11" and cof[("255", "dense")] == "3x5x17"
