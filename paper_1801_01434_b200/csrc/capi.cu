@@ -46,11 +46,39 @@ int sm_count()
     return cached > 0 ? cached : 148;
 }
 
+// Keep the stream-ordered pool's memory mapped between calls: with the default
+// release threshold (0) every multi-GiB scratch buffer is unmapped at the next
+// synchronisation and re-mapped by the next call (seconds at 16 GiB).
+static void keep_pool_mapped()
+{
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+
 int scratch_alloc(Scratch &s, size_t bytes, cudaStream_t st)
 {
+    keep_pool_mapped();
     s.st = st;
     if (bytes == 0) bytes = 16;
     cudaError_t e = cudaMallocAsync(&s.ptr, bytes, st);
+    if (e == cudaErrorMemoryAllocation) {
+        // give cached pool memory back (e.g. a previous q = 2^32 call) and retry once
+        cudaGetLastError();
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            cudaStreamSynchronize(st);
+            cudaMemPoolTrimTo(pool, 0);
+        }
+        e = cudaMallocAsync(&s.ptr, bytes, st);
+    }
     if (e != cudaSuccess) {
         s.ptr = nullptr;
         return check_cuda(e, "cudaMallocAsync(scratch)");
