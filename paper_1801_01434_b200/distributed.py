@@ -237,3 +237,98 @@ def dump_spectrum_sharded(out, q: int, path, *, rank: int = 0, world: int = 1, g
     if world > 1:
         import torch.distributed as dist
         dist.barrier(group=group)
+
+
+def sampler_at(seed: int, draws: int) -> qstate.Sampler:
+    """A Sampler positioned `draws` uniforms into seed's stream (PCG64.advance).
+
+    Generator.random() consumes exactly one 64-bit PCG64 output per double."""
+    s = qstate.Sampler(seed)
+    if draws:
+        s._gen.bit_generator.advance(draws)
+    return s
+
+
+def concurrent_attempts(cfg, *, rank: int = 0, world: int = 1, group=None, attempt_fn=None):
+    """The attempt loop of shor.run_shor (shor.py:155-166) with attempts run
+    concurrently, one per rank -- and still the reference's exact trace.
+
+    Every attempt that does not end the loop consumes exactly the same number
+    of draws (x, u_k, u_m; or u_k, u_m with base_override), and the one that
+    ends it is the first success, so attempt i starts at draw i*per_attempt of
+    the seed's stream regardless of what earlier attempts measured.  Rank g
+    runs attempts g, g+G, ...; after each round the traces are exchanged and
+    the loop stops at the lowest-index success.  Returns (attempts, parts).
+    """
+    import time as _time
+
+    from . import numtheory as nt
+    from . import shor
+    attempt_fn = attempt_fn or shor.single_attempt
+    per = 2 if cfg.base_override is not None else 3
+    t0 = _time.perf_counter()
+    deadline = None if cfg.time_budget is None else t0 + cfg.time_budget
+    attempts, parts = [], None
+    base = 0
+    while base < cfg.max_attempts and parts is None:
+        if deadline is not None and _time.perf_counter() >= deadline:
+            break
+        i = base + rank
+        mine = attempt_fn(cfg, sampler_at(cfg.seed, per * i)) if i < cfg.max_attempts else None
+        if world > 1:
+            import torch.distributed as dist
+            got = [None] * world
+            dist.all_gather_object(got, mine, group=group)
+        else:
+            got = [mine]
+        for tr in got:
+            if tr is None:
+                continue
+            attempts.append(tr)
+            if tr.outcome.kind == "classical_shortcut":
+                parts = [tr.outcome.shortcut, cfg.n // tr.outcome.shortcut]
+                break
+            if tr.outcome.kind == "factors":
+                parts = list(tr.outcome.factors)
+                break
+        base += world
+    del nt
+    return attempts, parts
+
+
+def run_shor_concurrent(cfg, *, rank: int = 0, world: int = 1, group=None, attempt_fn=None):
+    """shor.run_shor with the top-level attempts spread over the ranks (one full
+    attempt per GPU at a time).  Same ShorResult as the sequential driver:
+    identical attempt traces, factors and recursion (child seeds derived as in
+    shor.py:174-195; cofactors are factored sequentially on every rank)."""
+    import time as _time
+    from dataclasses import replace as _replace
+
+    from . import numtheory as nt
+    from . import shor
+    t_start = _time.perf_counter()
+    if cfg.n < 3:
+        raise ValueError("n must be >= 3")
+    shortcut = nt.pre_checks(cfg.n)
+    if shortcut is not None:
+        attempts, parts = [], list(shortcut.factors)
+    else:
+        attempts, parts = concurrent_attempts(cfg, rank=rank, world=world, group=group, attempt_fn=attempt_fn)
+    if parts is None:
+        return shor.ShorResult(n=cfg.n, factors=[], attempts=attempts,
+                               total_time=_time.perf_counter() - t_start, succeeded=False)
+    primes = []
+    for part in parts:
+        if nt.is_prime(part):
+            primes.append(part)
+            continue
+        budget = None if cfg.time_budget is None else max(cfg.time_budget - (_time.perf_counter() - t_start), 0.0)
+        sub = shor.run_shor(_replace(cfg, n=part, seed=shor._derive_seed(cfg.seed, part), base_override=None,
+                                     time_budget=budget, dump_state_path=None))
+        attempts.extend(sub.attempts)
+        if not sub.succeeded:
+            return shor.ShorResult(n=cfg.n, factors=[], attempts=attempts,
+                                   total_time=_time.perf_counter() - t_start, succeeded=False)
+        primes.extend(sub.factors)
+    return shor.ShorResult(n=cfg.n, factors=sorted(primes), attempts=attempts,
+                           total_time=_time.perf_counter() - t_start, succeeded=True)

@@ -70,3 +70,33 @@ def test_random_weights_seqsum(lib):
         n = int(rng.integers(1, 200000))
         assert nat.host_seqsum_const(w, n) == np.cumsum(np.full(n, w))[-1]
         assert nat.host_pairwise_sum_const(w, n) == np.full(n, w).sum()
+
+
+def test_abi_argument_errors_without_device(lib):
+    import ctypes
+    E = nat.SHB_EINVAL
+    d = ctypes.c_double(0)
+    u = ctypes.c_uint64(0)
+    assert lib.shb_modexp(None, 0, 16, 2, 1, None) == E                      # modulus < 2
+    assert lib.shb_modexp(None, 0, 16, 2, 1 << 33, None) == E                # > 32-bit residues
+    assert b"32-bit" in lib.shb_last_error()
+    assert lib.shb_class_counts(None, 16, None, 0, None) == E                # ncls == 0
+    args = (None, 4, 0, 1, 1000, 0, 1000, 1, 1.0, 0, None, None, None, None)  # q not a power of two
+    assert lib.shb_dft(*args) == E and b"power of two" in lib.shb_last_error()
+    assert lib.shb_dft(None, 4, 0, 1, 1024, 0, 1024, 3, 1.0, 0, None, None, None, None) == E   # tiles
+    assert lib.shb_dft(None, 4, 1020, 2, 1024, 0, 1024, 1, 1.0, 0, None, None, None, None) == E  # leaves [0,q)
+    assert lib.shb_dft(None, 4, 0, 1, 1024, 1000, 100, 1, 1.0, 0, None, None, None, None) == E   # rows
+    assert lib.shb_dft(None, 4, 0, 1, 1024, 0, 8, 1, 1.0, 7, None, None, None, None) == E        # precision
+    assert lib.shb_dft_uniform(1.0, 0.0, 4, 0, 0, 1024, 0, 8, 1, 1.0, 0, None, None, None, None) == E  # stride 0
+    assert lib.shb_dense_dft_host(None, 1024, 1, 0, None) == E
+    assert lib.shb_partial_row_sums_host(None, None, None, 1024, 0, 8, 0, 8) == E
+    assert lib.shb_sum(None, 0, None, None) == E
+    assert lib.shb_cumsum_search(None, 0, 0.5, None, None) == E
+    assert lib.shb_sample_index(None, 0, 0.5, ctypes.byref(u), ctypes.byref(d), None) == nat.SHB_OK
+    assert u.value == 0  # empty input: index = count = 0
+    with pytest.raises(ValueError):
+        nat.check(E, "x")
+    with pytest.raises(MemoryError):
+        nat.check(nat.SHB_ENOMEM, "x")
+    with pytest.raises(RuntimeError):
+        nat.check(nat.SHB_ECUDA, "x")

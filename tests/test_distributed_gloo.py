@@ -147,3 +147,56 @@ def test_single_rank_matches_reference_traces(single, golden_dir):
     tr = ref[(221, 0, None)]["attempts"]
     got = single[1]
     assert [(a["x"], a["k"], a["m"]) for a in got] == [(t["x"], t["k"], t["m"]) for t in tr]
+
+
+def _oracle_attempt(cfg, sampler):
+    """single_attempt with the oracle as the stage ops (test-only, world=1 inside)."""
+    from paper_1801_01434_b200 import numtheory as nt
+    x = cfg.base_override if cfg.base_override is not None else shor._draw_base(cfg.n, sampler)
+    g = math.gcd(x, cfg.n)
+    if g > 1:
+        return shor.AttemptTrace(x=x, q=None, k=None, m=None, candidate=None,
+                                 outcome=nt.FactorOutcome.classical(g), phase_times={})
+    q = nt.choose_register_width(cfg.n, cfg.max_width).q
+    r = D.sharded_attempt(cfg.n, x, q, sampler, ops=OracleOps())
+    est = nt.extract_period(r.m, q, cfg.n, x, cfg.multiplier_cap)
+    cand = est if isinstance(est, nt.PeriodCandidate) else None
+    out = nt.derive_factors(cfg.n, x, est.p) if cand else est
+    return shor.AttemptTrace(x=x, q=q, k=r.k, m=r.m, candidate=cand, outcome=out, phase_times={})
+
+
+def _concurrent_worker(rank, world, port, cases, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        for n, seed in cases:
+            cfg = shor.ShorConfig(n=n, seed=seed, kernel="dense")
+            atts, parts = D.concurrent_attempts(cfg, rank=rank, world=world, attempt_fn=_oracle_attempt)
+            out.append(([(a.x, a.k, a.m, a.outcome.kind) for a in atts], parts))
+        ret[rank] = out
+    finally:
+        dist.destroy_process_group()
+
+
+def test_concurrent_attempts_reproduce_sequential_trace(golden_dir):
+    """Rank-parallel attempts reproduce the reference's sequential attempt trace exactly."""
+    kats = json.loads((golden_dir / "kats.json").read_text())
+    cases = [(r["n"], r["cfg"]["seed"]) for r in kats["traces"]
+             if r["cfg"].get("kernel") == "dense" and "base_override" not in r["cfg"] and r["n"] <= 221]
+    ctx = mp.get_context("spawn")
+    ret = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_concurrent_worker, args=(r, 3, port, cases, ret)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    ref = {(r["n"], r["cfg"]["seed"]): r for r in kats["traces"]}
+    for (n, seed), (atts, parts) in zip(cases, ret[0]):
+        want = ref[(n, seed)]
+        top = [a for a in want["attempts"]][:len(atts)]
+        assert [(a[0], a[1], a[2]) for a in atts] == [(t["x"], t["k"], t["m"]) for t in top], (n, seed)
+        assert sorted(parts) == sorted(want["factors"][:2]) or want["n"] != n
+        assert ret[1] == ret[0] and ret[2] == ret[0]
