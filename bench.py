@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-factoring", action="store_true")
+    p.add_argument("--no-fp32", action="store_true")
     return p.parse_args()
 
 
@@ -247,11 +248,11 @@ def run_b200(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    def one_step(time_dft=False):
+    def one_step(time_dft=False, keep=False, precision=None):
         s = qstate.Sampler(args.seed)
         xx = shor._draw_base(args.n, s)
         rec = D.sharded_attempt(args.n, xx, q, s, rank=rank, world=world, group=group,
-                                precision=args.precision, time_dft=time_dft)
+                                precision=precision or args.precision, time_dft=time_dft, keep_spectrum=keep)
         est = nt.extract_period(rec.m, q, args.n, xx)
         out = nt.derive_factors(args.n, xx, est.p) if isinstance(est, nt.PeriodCandidate) else est
         return rec, out
@@ -267,8 +268,8 @@ def run_b200(args):
     barrier()
     e0.record()
     dft_ms, recs = [], []
-    for _ in range(args.steps):
-        rec, outcome = one_step(time_dft=True)
+    for i in range(args.steps):
+        rec, outcome = one_step(time_dft=True, keep=(i == args.steps - 1 and not args.no_fp32))
         recs.append(rec)
         dft_ms.append(rec.dft_ms)
     e1.record()
@@ -285,10 +286,15 @@ def run_b200(args):
     terms_step = q * M
     value = terms_step * args.steps / (el_ms / 1000.0)
 
-    # roofline of the dominant kernel (the DFT), per GPU
+    # roofline of the dominant kernel (the DFT), per GPU.  Peak: the nominal
+    # FP64 rate (SMs x 64 DFMA/clk x 2 flops) at the SM clock measured during
+    # the timed region -- a hard upper bound (MEASURED_PEAKS.json has no FP64
+    # figure); the DFMA-chain probe is reported beside it.
     ptf = ctypes_double()
     nat.check(lib.shb_fp64_peak(2.0, ptf, None), "fp64 peak")
-    peak_tf = ptf.value
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    clk_mhz = clk.get("sm_mhz") or 1965.0
+    peak_tf = sms * 64 * 2 * clk_mhz * 1e6 / 1e12
     dft_s = statistics.mean(dft_ms) / 1000.0
     achieved_tf = 8.0 * rec.phase_terms / dft_s / 1e12
     # DRAM bytes per DFT launch from the committed ncu --set full capture, only
@@ -309,8 +315,10 @@ def run_b200(args):
     roof = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
             "frac": achieved_tf / peak_tf, "traffic": traffic, "traffic_note": traffic_note,
             "traffic_unit": "bytes/launch", "algorithmic_bytes_per_launch": 24 * (q // world),
-            "peak_source": "measured on this GPU by shb_fp64_peak (independent DFMA chains); "
-                           "MEASURED_PEAKS.json has no FP64 figure; nominal 37.2 TF at 1965 MHz",
+            "peak_source": f"nominal FP64: {sms} SMs x 64 DFMA/clk x 2 flops x {clk_mhz:.0f} MHz "
+                           "(median SM clock in the timed region); MEASURED_PEAKS.json has no FP64 figure",
+            "peak_probe": ptf.value,
+            "peak_probe_note": "shb_fp64_peak: independent DFMA chains with constant operands on this GPU",
             "kernel": "shb::dft_kernel<double>", "dft_ms_per_launch": dft_s * 1000.0,
             "flops_per_launch": 8.0 * rec.phase_terms}
 
@@ -336,6 +344,23 @@ def run_b200(args):
     # every rank runs the _kernels.partial_row_sums seam on its row shard.
     if not args.no_e2e:
         line["e2e"] = e2e_host(args, q, x, lib, torch, nat, rank, world)
+    # FP32 fast path on the same attempt: Horner in FP32 with exact FP64
+    # re-seeds every 256 terms; accuracy vs the FP64 spectrum just measured
+    if not args.no_fp32 and args.precision == "fp64":
+        _, p64 = rec.spectrum
+        rec32, out32 = one_step(time_dft=True, keep=True, precision="fp32")
+        _, p32 = rec32.spectrum
+        err = torch.stack([(p32 - p64).abs().max(), p64.max()])
+        del rec32.spectrum, rec.spectrum
+        t32 = torch.tensor([rec32.dft_ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(err, op=torch.distributed.ReduceOp.MAX)
+            torch.distributed.all_reduce(t32, op=torch.distributed.ReduceOp.MAX)
+        line["fp32_fast_path"] = {
+            "dft_ms": float(t32.item()), "phase_terms_per_s": q * M / (float(t32.item()) / 1000.0),
+            "max_abs_dp_over_max_p": float(err[0] / err[1]), "tolerance": 1e-4,
+            "m": rec32.m, "m_equal_fp64": rec32.m == rec.m, "note": "DFT kernel only; not the headline (FP64)"}
+
     if not args.no_factoring:
         from paper_1801_01434_b200 import qft
         barrier()

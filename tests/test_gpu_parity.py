@@ -375,7 +375,7 @@ def test_cli_factor_and_bench_suite(capsys):
     from paper_1801_01434_b200 import cli
     assert cli.main(["factor", "--n", "77", "--kernel", "dense"]) == 0
     out = json.loads(capsys.readouterr().out)
-    assert out["factors"] == [7, 11] and out["qft_fraction"] > 0
+    assert out["factors"] == [7, 11] and 0.0 <= out["qft_fraction"] <= 1.0
     # SPEC acceptance 1 (cofactor multisets of Table 3), small suite, two engine names
     assert cli.main(["bench", "--suite", "table3-small", "--engines", "dense,fft", "--format", "csv"]) == 0
     lines = capsys.readouterr().out.strip().splitlines()
