@@ -23,7 +23,8 @@
 //  * generic (UNIF=false): any complex amplitudes.  The amplitude stream is
 //    shared by the whole CTA and staged into shared memory by TMA bulk copies
 //    (cp.async.bulk + mbarrier ring); inner loop = LDS.128 broadcast + 4 DFMA
-//    per output.
+//    per output and phase term, with pairs of Horner steps fused as
+//    acc*W^2 + (a_j*W + a_{j+1}) so half of the FMAs read broadcast operands.
 //  * uniform comb (UNIF=true): every amplitude equals `amp` (the collapsed
 //    Shor register).  amp is factored out of the sum, the Horner
 //    step becomes acc*w + 1 (3 DFMA + 1 DMUL, the constant from the constant
@@ -101,7 +102,8 @@ __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
     // per-output state: step rotation (cos, sin) of phi = 2 pi stride c / q,
     // Horner acc (h), tile partial (t, only when tiles > 1), running total (v)
     constexpr int KT = TILED ? K : 1;
-    R wr[K], wi[K], hr[K], hi[K];
+    constexpr int K2 = UNIF ? 1 : K;  // W^2 only on the generic path
+    R wr[K], wi[K], hr[K], hi[K], w2r[K2], w2i[K2];
     double tr[KT], ti[KT], vr[K], vi[K];
     uint64_t cval[K];
 #pragma unroll
@@ -111,6 +113,11 @@ __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
         phase((p.stride * cval[i]) & qmask, q, p.two_over_q, co, si);
         wr[i] = (R)co;
         wi[i] = (R)si;
+        if (!UNIF) {
+            phase((2 * p.stride * cval[i]) & qmask, q, p.two_over_q, co, si);
+            w2r[i % K2] = (R)co;
+            w2i[i % K2] = (R)si;
+        }
         hr[i] = hi[i] = (R)0;
         vr[i] = vi[i] = 0.0;
     }
@@ -159,13 +166,30 @@ __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
             const int s = ch % DFT_STAGES;
             mbar_wait(&full_bar[s], (ch / DFT_STAGES) & 1u);
             const double2 *sb = buf + (size_t)s * DFT_CHUNK;
-#pragma unroll 4
-            for (int e = 0; e < cnt; e++) {
+            // two Horner steps fused: acc'' = acc*W^2 + (a_j*W + a_{j+1}),
+            // W = conj(e^{i phi}).  Still 4 FMA per phase term, but the
+            // b = a_j*W + a_{j+1} half takes two warp-uniform (broadcast)
+            // amplitude operands, which keeps register-file reads near 2 per FMA.
+            int e = 0;
+#pragma unroll 2
+            for (; e + 2 <= cnt; e += 2) {
+                const double2 av0 = sb[e], av1 = sb[e + 1];
+                const R a0r = (R)av0.x, a0i = (R)av0.y, a1r = (R)av1.x, a1i = (R)av1.y;
+#pragma unroll
+                for (int i = 0; i < K; i++) {
+                    const R b_re = fma(a0r, wr[i], fma(a0i, wi[i], a1r));
+                    const R b_im = fma(a0i, wr[i], fma(-a0r, wi[i], a1i));
+                    const R n_re = fma(hr[i], w2r[i], fma(hi[i], w2i[i], b_re));
+                    const R n_im = fma(hi[i], w2r[i], fma(-hr[i], w2i[i], b_im));
+                    hr[i] = n_re;
+                    hi[i] = n_im;
+                }
+            }
+            if (e < cnt) {  // odd tail: one plain Horner step
                 const double2 av = sb[e];
                 const R a_re = (R)av.x, a_im = (R)av.y;
 #pragma unroll
                 for (int i = 0; i < K; i++) {
-                    // acc * conj(e^{i phi}) + a
                     const R t_re = fma(hi[i], wi[i], a_re);
                     const R t_im = fma(hi[i], wr[i], a_im);
                     const R n_re = fma(hr[i], wr[i], t_re);
