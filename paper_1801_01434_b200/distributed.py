@@ -262,7 +262,6 @@ def concurrent_attempts(cfg, *, rank: int = 0, world: int = 1, group=None, attem
     """
     import time as _time
 
-    from . import numtheory as nt
     from . import shor
     attempt_fn = attempt_fn or shor.single_attempt
     per = 2 if cfg.base_override is not None else 3
@@ -292,7 +291,6 @@ def concurrent_attempts(cfg, *, rank: int = 0, world: int = 1, group=None, attem
                 parts = list(tr.outcome.factors)
                 break
         base += world
-    del nt
     return attempts, parts
 
 
