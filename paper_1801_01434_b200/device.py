@@ -311,8 +311,9 @@ class CollapsedAmplitudes(DeviceVector):
 class DeviceSpectrum(DeviceVector):
     """A complex128 vector on the device (the QFT output), with |.|^2 fused."""
 
-    def __init__(self, q: int, data, prob=None, block_sums=None):
+    def __init__(self, q: int, data, prob=None, block_sums=None, precision: str = "fp64"):
         super().__init__(q)
+        self.precision = precision
         self.data = data  # float64 [2q] interleaved
         self.prob = prob  # float64 [q] = hypot(re, im)^2, or None
         self.block_sums = block_sums

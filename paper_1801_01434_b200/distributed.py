@@ -179,7 +179,7 @@ def sharded_attempt(n: int, x: int, q: int, sampler: qstate.Sampler, *, rank: in
         nt = torch.tensor([norm2], dtype=torch.float64, device=bsum.device)
         dist.all_reduce(nt, group=group)
         norm2 = float(nt.item())
-    if abs(math.sqrt(norm2) - 1.0) > 1e-9:
+    if abs(math.sqrt(norm2) - 1.0) > qstate.norm_tolerance(precision):
         raise ValueError(f"register is not normalized (|amp| = {math.sqrt(norm2)!r})")
     # (4) probability shards -> rank 0 -> exact sequential CDF -> m to all ranks
     u = sampler.uniform()

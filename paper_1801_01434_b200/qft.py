@@ -145,7 +145,7 @@ def _run(state, q: int, tiles: int, precision: str):
     else:
         out, prob, bsum = dev.dft(amps, length, a0, stride, q, 0, q, tiles=tiles,
                                   scale=1.0 / math.sqrt(q), precision=precision)
-    spec = dev.DeviceSpectrum(q, out, prob, bsum)
+    spec = dev.DeviceSpectrum(q, out, prob, bsum, precision=precision)
     return spec.numpy() if host else spec
 
 

@@ -381,3 +381,36 @@ def test_cli_factor_and_bench_suite(capsys):
     lines = capsys.readouterr().out.strip().splitlines()
     cof = {(ln.split(",")[0], ln.split(",")[2]): ln.split(",")[1] for ln in lines[1:]}
     assert cof[("77", "dense")] == "7x11" and cof[("231", "fft")] == "3x7x11" and cof[("255", "dense")] == "3x5x17"
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_exponent_shards_reassemble_bitwise(world):
+    """What each rank of distributed.sharded_attempt computes on its a-slice:
+    residues, accumulated class counts and offset compactions reassemble to the
+    single-GPU results exactly."""
+    from paper_1801_01434_b200 import distributed as D
+    x, n, q = 8477, 32399, 1 << 22
+    full = dev.modexp(x, n, q)
+    counts_full = dev.class_counts(full, n)
+    k = int(full[12345].item()) & 0xFFFFFFFF
+    sup_full = dev.compact_eq(full, k)
+    counts = torch.zeros(n, dtype=torch.int64, device="cuda")
+    sups = []
+    for g in range(world):
+        lo, hi = D.shard(q, g, world)
+        res = dev.modexp(x, n, hi - lo, a_begin=lo)
+        assert torch.equal(res, full[lo:hi])
+        dev.class_counts(res, n, out=counts)  # accumulates, like the all_reduce
+        sups.append(dev.compact_eq(res, k, a_begin=lo))
+    assert torch.equal(counts, counts_full)
+    assert torch.equal(torch.cat(sups), sup_full)
+    assert dev.support_progression(torch.cat(sups)) == dev.support_progression(sup_full)
+
+
+def test_fp32_pipeline_end_to_end():
+    # the FP32 fast path through the public API: same k, m and factors as FP64
+    res64 = shor.run_shor(shor.ShorConfig(n=3127, seed=0, kernel="dense", max_width=32))
+    res32 = shor.run_shor(shor.ShorConfig(n=3127, seed=0, kernel="dense", max_width=32,
+                                          plan=qft.KernelPlan(precision="fp32")))
+    assert res32.factors == res64.factors == [53, 59]
+    assert [(a.k, a.m) for a in res32.attempts] == [(a.k, a.m) for a in res64.attempts]
