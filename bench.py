@@ -225,12 +225,18 @@ def run_b200(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     group = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink in production; SHB_DIST_BACKEND=gloo lets a test put
+        # several ranks on one GPU (independent kernels, host-staged collectives)
+        backend = os.environ.get("SHB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_1801_01434_b200 import _native as nat
     from paper_1801_01434_b200 import build as buildmod
     from paper_1801_01434_b200 import distributed as D

@@ -417,3 +417,56 @@ def test_fp32_pipeline_end_to_end():
                                           plan=qft.KernelPlan(precision="fp32")))
     assert res32.factors == res64.factors == [53, 59]
     assert [(a.k, a.m) for a in res32.attempts] == [(a.k, a.m) for a in res64.attempts]
+
+
+def _two_rank_worker(rank, world, port, ret):
+    import os
+    import torch.distributed as dist
+    from paper_1801_01434_b200 import distributed as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s = qstate.Sampler(0)
+        x = shor._draw_base(3127, s)
+        rec = D.sharded_attempt(3127, x, 1 << 24, s, rank=rank, world=world, keep_spectrum=True)
+        out, _ = rec.spectrum
+        lo, hi = D.shard(1 << 24, rank, world)
+        rows = torch.tensor([0, 1, 144631, 578525, 12345678], device="cuda")
+        rows = rows[(rows >= lo) & (rows < hi)] - lo
+        ret[rank] = {"x": x, "k": rec.k, "m": rec.m, "M": rec.M, "r": rec.r, "c0": rec.c0,
+                     "rows": (rows + lo).tolist(),
+                     "vals": out.view(torch.complex128)[rows].cpu().numpy().view(np.float64).tolist()}
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_attempt_two_ranks_on_device():
+    """distributed.sharded_attempt with the real device kernels, 2 ranks on one
+    GPU (gloo collectives: host-staged; the kernels never wait on each other).
+    Same k, m, support and bitwise-identical spectrum rows as 1 rank."""
+    import socket
+
+    import torch.multiprocessing as mp
+    from paper_1801_01434_b200 import distributed as D
+    s = qstate.Sampler(0)
+    x = shor._draw_base(3127, s)
+    one = D.sharded_attempt(3127, x, 1 << 24, s, keep_spectrum=True)
+    full, _ = one.spectrum
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    ret = ctx.Manager().dict()
+    procs = [ctx.Process(target=_two_rank_worker, args=(r, 2, port, ret)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+        assert p.exitcode == 0
+    for r in range(2):
+        g = ret[r]
+        assert (g["k"], g["m"], g["M"], g["r"], g["c0"]) == (one.k, one.m, one.M, one.r, one.c0) == \
+            (825, 578525, 144631, 116, 29)
+        ref = full.view(torch.complex128)[torch.tensor(g["rows"], device="cuda")].cpu().numpy().view(np.float64)
+        assert np.array_equal(np.asarray(g["vals"]), ref)
