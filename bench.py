@@ -40,7 +40,7 @@ def parse():
     p.add_argument("--steps", type=int, default=2)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--n", type=int, default=32399)
+    p.add_argument("--modulus", dest="n", type=int, default=32399)  # not --n: torchrun prefix-matches it
     p.add_argument("--seed", type=int, default=8)
     p.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     p.add_argument("--max-width", type=int, default=32)

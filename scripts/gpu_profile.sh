@@ -5,7 +5,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 tail -5 gpurun_out/pytest_gpu.log
 timeout 300 python scripts/step_breakdown.py 32399 8 > gpurun_out/breakdown.log 2>&1; echo breakdown=$?
 cat gpurun_out/breakdown.log
-CMD="python bench.py --n 3127 --seed 0 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-factoring"
+CMD="python bench.py --modulus 3127 --seed 0 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-factoring"
 timeout 600 $CMD > gpurun_out/plain_3127.json 2> gpurun_out/plain_3127.err && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_3127.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo ncu_launches=$?
 cat gpurun_out/plain_3127.json
