@@ -48,7 +48,9 @@ struct ChunkDesc {
     uint32_t flags;
 };
 
-constexpr int DFT_THREADS = 256;
+constexpr int DFT_THREADS = 256;                    // consumer threads (own the outputs)
+constexpr int DFT_CONSUMER_WARPS = DFT_THREADS / 32;
+constexpr int DFT_PRODUCER_THREADS = 32;            // generic path: one TMA producer warp
 constexpr int DFT_STAGES = 4;
 constexpr int DFT_CHUNK = 1024;  // amplitudes per stage (16 KB)
 
@@ -87,12 +89,15 @@ struct DftArgs {
 };
 
 template <typename R, bool UNIF, bool TILED>
-__global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
+__global__ void __launch_bounds__(UNIF ? DFT_THREADS : DFT_THREADS + DFT_PRODUCER_THREADS,
+                                  (UNIF || !TILED) ? 2 : 1)
+    dft_kernel(const DftArgs p)
 {
     constexpr int K = Prec<R>::K;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *buf = reinterpret_cast<double2 *>(smem_raw);
     __shared__ __align__(8) uint64_t full_bar[DFT_STAGES];
+    __shared__ __align__(8) uint64_t empty_bar[DFT_STAGES];
     __shared__ double red_tmp[DFT_THREADS / 32];
 
     const int tid = threadIdx.x;
@@ -124,27 +129,34 @@ __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
 #pragma unroll
     for (int i = 0; i < KT; i++) tr[i] = ti[i] = 0.0;
 
+    // generic path: warp-specialised pipeline.  The warp after the 8 consumer
+    // warps is the TMA producer; full_bar[s] completes when stage s holds its
+    // chunk (tx bytes), empty_bar[s] when all consumer warps are done with it,
+    // so consumer warps never wait on each other.
     if (!UNIF) {
         if (tid == 0) {
 #pragma unroll
-            for (int s = 0; s < DFT_STAGES; s++) mbar_init(&full_bar[s], 1);
+            for (int s = 0; s < DFT_STAGES; s++) {
+                mbar_init(&full_bar[s], 1);
+                mbar_init(&empty_bar[s], DFT_CONSUMER_WARPS);
+            }
             fence_mbar_init();
         }
         __syncthreads();
+        if (tid == DFT_THREADS) {
+            for (uint32_t ch = 0; ch < p.nchunks; ch++) {
+                const int s = ch % DFT_STAGES;
+                if (ch >= DFT_STAGES) mbar_wait(&empty_bar[s], ((ch / DFT_STAGES) - 1) & 1u);
+                const ChunkDesc d = p.sched[ch];
+                const uint32_t bytes = d.cnt * 16u;
+                mbar_arrive_expect_tx(&full_bar[s], bytes);
+                tma_bulk_g2s(buf + (size_t)s * DFT_CHUNK, p.amps + d.j0, bytes, &full_bar[s]);
+            }
+        }
     }
-    auto issue = [&](uint32_t ch) {
-        const ChunkDesc d = p.sched[ch];
-        const int s = ch % DFT_STAGES;
-        const uint32_t bytes = d.cnt * 16u;
-        mbar_arrive_expect_tx(&full_bar[s], bytes);
-        tma_bulk_g2s(buf + (size_t)s * DFT_CHUNK, p.amps + d.j0, bytes, &full_bar[s]);
-    };
-    if (!UNIF && tid == 0) {
-        const uint32_t pro = p.nchunks < DFT_STAGES ? p.nchunks : DFT_STAGES;
-        for (uint32_t ch = 0; ch < pro; ch++) issue(ch);
-    }
+    const bool consumer = UNIF || tid < DFT_THREADS;  // the producer warp owns no outputs
 
-    for (uint32_t ch = 0; ch < p.nchunks; ch++) {
+    for (uint32_t ch = 0; consumer && ch < p.nchunks; ch++) {
         const ChunkDesc d = p.sched[ch];
         const int cnt = (int)d.cnt;
         if (UNIF) {
@@ -226,8 +238,8 @@ __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
             }
         }
         if (!UNIF) {
-            __syncthreads();  // every warp is done with stage s
-            if (tid == 0 && ch + DFT_STAGES < p.nchunks) issue(ch + DFT_STAGES);
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty_bar[ch % DFT_STAGES]);  // warp done with the stage
         }
     }
 
@@ -236,7 +248,7 @@ __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
 #pragma unroll
     for (int i = 0; i < K; i++) {
         const uint64_t ci = cblk + (uint64_t)i * DFT_THREADS + tid;
-        if (ci < p.c_count) {
+        if (consumer && ci < p.c_count) {
             const double o_re = vr[i] * p.out_re - vi[i] * p.out_im;
             const double o_im = vr[i] * p.out_im + vi[i] * p.out_re;
             p.out[ci] = make_double2(o_re, o_im);
@@ -249,7 +261,7 @@ __global__ void __launch_bounds__(DFT_THREADS, 2) dft_kernel(const DftArgs p)
     if (p.block_sums) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) psum += __shfl_down_sync(0xffffffffu, psum, o);
-        if ((tid & 31) == 0) red_tmp[tid >> 5] = psum;
+        if ((tid & 31) == 0 && consumer) red_tmp[tid >> 5] = psum;
         __syncthreads();
         if (tid == 0) {
             double b = 0.0;
@@ -307,7 +319,8 @@ static int launch_dft_t(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t
     const uint64_t per_blk = (uint64_t)DFT_THREADS * K;
     const uint64_t nblk = (a.c_count + per_blk - 1) / per_blk;
     if (nblk > 0x7FFFFFFFull) return set_error(SHB_EINVAL, "too many outputs for one launch");
-    dft_kernel<R, UNIF, TILED><<<(unsigned)nblk, DFT_THREADS, smem, st>>>(a);
+    const unsigned nthreads = UNIF ? DFT_THREADS : DFT_THREADS + DFT_PRODUCER_THREADS;
+    dft_kernel<R, UNIF, TILED><<<(unsigned)nblk, nthreads, smem, st>>>(a);
     SHB_LAUNCHED();
     SHB_TRY_CUDA(cudaGetLastError());
     return SHB_OK;

@@ -110,6 +110,11 @@ __device__ inline void mbar_wait(uint64_t *bar, uint32_t phase)
         : "memory");
 }
 
+__device__ inline void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
 // 1-D bulk copy global -> shared through the TMA unit (UBLKCP), completion
 // signalled on `bar` with complete_tx.  bytes % 16 == 0, 16-B aligned.
 __device__ inline void tma_bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes,
