@@ -427,24 +427,25 @@ def e2e_host(args, q, x, lib, torch, nat, rank=0, world=1):
     stn[:] = 0
     stn[c0::r] = amp
     prec = 0 if args.precision == "fp64" else 1
-    # warm the path once at a small size (allocator pools, schedule upload)
-    small = np.zeros(1024, dtype=np.complex128)
-    small[3::7] = 0.1
-    so = np.empty_like(small)
-    nat.check(lib.shb_dense_dft_host(ctypes.c_void_p(small.ctypes.data), 1024, 1, prec,
-                                     ctypes.c_void_p(so.ctypes.data)))
+    def call():
+        if world == 1:
+            nat.check(lib.shb_dense_dft_host(ctypes.c_void_p(st.data_ptr()), q, 1, prec,
+                                             ctypes.c_void_p(out.data_ptr())), "dense_dft_host")
+        else:
+            nat.check(lib.shb_partial_row_sums_host(ctypes.c_void_p(out.data_ptr()),
+                                                    ctypes.c_void_p(st.data_ptr()), None, q, c_lo, c_hi, 0, q),
+                      "partial_row_sums_host")
+
+    api = ("shb_dense_dft_host (C ABI of qft.dense_dft, pinned host buffers)" if world == 1 else
+           "shb_partial_row_sums_host (C ABI of _kernels.partial_row_sums), row shard per rank")
+    # one untimed call at full size: maps the library's stream-ordered pool
+    # (a one-off per process) so the timed call is the steady state
+    call()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
-    if world == 1:
-        nat.check(lib.shb_dense_dft_host(ctypes.c_void_p(st.data_ptr()), q, 1, prec,
-                                         ctypes.c_void_p(out.data_ptr())), "dense_dft_host")
-        api = "shb_dense_dft_host (C ABI of qft.dense_dft, pinned host buffers)"
-    else:
-        nat.check(lib.shb_partial_row_sums_host(ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.data_ptr()),
-                                                None, q, c_lo, c_hi, 0, q), "partial_row_sums_host")
-        api = "shb_partial_row_sums_host (C ABI of _kernels.partial_row_sums), row shard per rank"
+    call()
     el = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([el], dtype=torch.float64, device="cuda")
@@ -454,7 +455,7 @@ def e2e_host(args, q, x, lib, torch, nat, rank=0, world=1):
     v0 = o[0] if rank == 0 else complex(0)
     del st, out
     return {"value": q * M / el, "unit": UNIT, "h2d_bytes_per_step": 16 * q * world,
-            "d2h_bytes_per_step": 16 * q, "steps": 1, "seconds": el, "api": api,
+            "d2h_bytes_per_step": 16 * q, "steps": 1, "warmup": 1, "seconds": el, "api": api,
             "check_V0": [float(v0.real), float(v0.imag)]}
 
 
