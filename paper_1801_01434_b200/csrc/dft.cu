@@ -108,6 +108,13 @@ __global__ void __launch_bounds__(UNIF ? DFT_THREADS : DFT_THREADS + DFT_PRODUCE
     // Horner acc (h), tile partial (t, only when tiles > 1), running total (v)
     constexpr int KT = TILED ? K : 1;
     constexpr int K2 = UNIF ? 1 : K;  // W^2 only on the generic path
+    // FP32 path: segment seeds advance by the exact FP64 rotation U = e^{i phi SEG}
+    // between full consecutive segments, re-seeded by sincospi every SEED_EXACT
+    constexpr bool F32 = sizeof(R) == 4 && UNIF;  // the generic path keeps exact seeds (register budget)
+    constexpr int KS = F32 ? K : 1;
+    constexpr uint32_t SEED_EXACT = 32;
+    double sdr[KS], sdi[KS], ur[KS], ui[KS];
+    uint32_t segs_done = 0;
     R wr[K], wi[K], hr[K], hi[K], w2r[K2], w2i[K2];
     double tr[KT], ti[KT], vr[K], vi[K];
     uint64_t cval[K];
@@ -125,6 +132,12 @@ __global__ void __launch_bounds__(UNIF ? DFT_THREADS : DFT_THREADS + DFT_PRODUCE
         }
         hr[i] = hi[i] = (R)0;
         vr[i] = vi[i] = 0.0;
+        if (F32) {
+            phase((Prec<R>::SEG * p.stride * cval[i]) & qmask, q, p.two_over_q, co, si);
+            ur[i % KS] = co;
+            ui[i % KS] = si;
+            sdr[i % KS] = sdi[i % KS] = 0.0;
+        }
     }
 #pragma unroll
     for (int i = 0; i < KT; i++) tr[i] = ti[i] = 0.0;
@@ -214,10 +227,23 @@ __global__ void __launch_bounds__(UNIF ? DFT_THREADS : DFT_THREADS + DFT_PRODUCE
         if (d.flags & CH_SEG_END) {
             // seed = e^{+2 pi i a_last c / q}; t += seed * acc; acc = 0
             const uint64_t a_last = p.a0 + (d.j0 + d.cnt - 1) * p.stride;
+            // a full segment right after another one ends SEG*stride later: its
+            // seed is the previous seed times U (FP32 path; FP64 re-seeds exactly)
+            const bool exact = !F32 || segs_done % SEED_EXACT == 0 || d.cnt != Prec<R>::SEG;
+            segs_done++;
 #pragma unroll
             for (int i = 0; i < K; i++) {
                 double sc, ss;
-                phase((a_last * cval[i]) & qmask, q, p.two_over_q, sc, ss);
+                if (exact) {
+                    phase((a_last * cval[i]) & qmask, q, p.two_over_q, sc, ss);
+                } else {
+                    sc = fma(sdr[i % KS], ur[i % KS], -sdi[i % KS] * ui[i % KS]);
+                    ss = fma(sdr[i % KS], ui[i % KS], sdi[i % KS] * ur[i % KS]);
+                }
+                if (F32) {
+                    sdr[i % KS] = sc;
+                    sdi[i % KS] = ss;
+                }
                 const double xr = (double)hr[i], xi = (double)hi[i];
                 if (TILED) {
                     tr[i % KT] = fma(sc, xr, fma(-ss, xi, tr[i % KT]));
