@@ -470,3 +470,46 @@ def test_sharded_attempt_two_ranks_on_device():
             (825, 578525, 144631, 116, 29)
         ref = full.view(torch.complex128)[torch.tensor(g["rows"], device="cuda")].cpu().numpy().view(np.float64)
         assert np.array_equal(np.asarray(g["vals"]), ref)
+
+
+def test_edge_cases_vs_oracle():
+    rng = np.random.default_rng(11)
+    # smallest register, basis and random states
+    for st in ([1, 0], [0, 1], [0.6, 0.8j]):
+        z = np.asarray(st, dtype=np.complex128)
+        got = qft.dense_dft(z, qft.build_twiddles(2), qft.KernelPlan())
+        assert np.max(np.abs(got - oracle.dense_dft(z))) < 1e-15
+    # all-zero state -> zeros; single element at the last index (progression length 1)
+    q = 1 << 12
+    assert not np.any(qft.dense_dft(np.zeros(q, complex), qft.build_twiddles(q), qft.KernelPlan()))
+    z = np.zeros(q, complex)
+    z[q - 1] = 1j
+    assert np.max(np.abs(qft.dense_dft(z, qft.build_twiddles(q), qft.KernelPlan()) - oracle.dense_dft(z))) < 1e-14
+    # support with holes (gcd stride 3, one zero slot) -> generic kernel
+    z = np.zeros(q, complex)
+    z[[1, 4, 10, 4000]] = rng.standard_normal(4) + 1j * rng.standard_normal(4)
+    for tiles in (1, 2, 16, q):
+        plan = qft.KernelPlan(tiles=tiles)
+        fn = qft.dense_dft if tiles == 1 else qft.tiled_dft
+        ref = oracle.dense_dft(z) if tiles == 1 else oracle.tiled_dft(z, tiles)
+        assert np.max(np.abs(fn(z, qft.build_twiddles(q), plan) - ref)) < 1e-13, tiles
+    # ragged output ranges on both kernels (partial CTAs)
+    sup = torch.arange(100, dtype=torch.int64, device="cuda") * 7 + 3
+    amps = dev.fill_progression(sup, 100, 3, 7, 100, 0.1 + 0.2j)
+    for lo, cnt in [(0, 1), (5, 1023), (999, 1025), (q - 3, 3)]:
+        out, _, _ = dev.dft(amps, 100, 3, 7, q, lo, cnt)
+        ou, _, _ = dev.dft_uniform(0.1 + 0.2j, 100, 3, 7, q, lo, cnt)
+        ref = oracle.dft_rows(3 + 7 * np.arange(100, dtype=np.uint64), np.full(100, 0.1 + 0.2j), q,
+                              np.arange(lo, lo + cnt, dtype=np.uint64))
+        assert np.max(np.abs(out.cpu().numpy().view(np.complex128) - ref)) < 1e-14
+        assert np.max(np.abs(ou.cpu().numpy().view(np.complex128) - ref)) < 1e-14
+
+
+def test_modexp_edge_bases():
+    # x >= n reduces mod n; x = 1 gives all ones; n = 2 (every residue 1)
+    assert np.array_equal(dev.modexp(15 + 7, 15, 64).cpu().numpy(), oracle.modexp_residues(7, 15, 64).view(np.int32))
+    assert np.all(dev.modexp(1, 15, 100).cpu().numpy() == 1)
+    assert np.all(dev.modexp(3, 2, 50).cpu().numpy() == 1)
+    reg = qstate.entangle_modexp(qstate.init_uniform(8), 1, 15)
+    k, rc = qstate.measure_part2(reg, Forced([0.5]))
+    assert k == 1 and rc.amplitudes.m == 8 and abs(qstate.l2_norm(rc) - 1) < 1e-15
