@@ -513,3 +513,28 @@ def test_modexp_edge_bases():
     reg = qstate.entangle_modexp(qstate.init_uniform(8), 1, 15)
     k, rc = qstate.measure_part2(reg, Forced([0.5]))
     assert k == 1 and rc.amplitudes.m == 8 and abs(qstate.l2_norm(rc) - 1) < 1e-15
+
+
+@pytest.mark.parametrize("tag,n,attempt,q", [("n3127", 3127, 1, 1 << 24), ("n221", 221, 2, 1 << 16)])
+def test_sampled_m_matches_reference_over_1000_draws(golden_dir, tag, n, attempt, q):
+    """m over 1000 random draws equals the reference's m on the reference's own
+    spectrum (fft engine at 2^24, dense at 2^16): our spectrum differs at ~1e-13
+    and our cumsum is the exact sequential emulation, so no draw flips.  The 60
+    adversarial draws placed within one ulp of peak CDF boundaries are reported."""
+    d = np.load(golden_dir / "sampling_sweep.npz")
+    s = qstate.Sampler(0)
+    for a in range(attempt):
+        x = shor._draw_base(n, s)
+        reg = qstate.entangle_modexp(qstate.init_uniform(q), x, n)
+        k, rc = qstate.measure_part2(reg, s)
+        if a < attempt - 1:
+            s.uniform()
+    assert (x, k) == (int(d[f"{tag}_x"]), int(d[f"{tag}_k"]))
+    spec = qft.transform(rc.amplitudes, "dense", qft.build_twiddles(q), qft.KernelPlan())
+    p = spec.probabilities()
+    us, ms = d[f"{tag}_u"], d[f"{tag}_m"]
+    got = np.array([min(dev.sample_index(p, float(u))[0], q - 1) for u in us])
+    assert np.array_equal(got[:1000], ms[:1000])
+    boundary_flips = int(np.sum(got[1000:] != ms[1000:]))
+    print(f"{tag}: 1000/1000 random draws equal; boundary-adversarial flips {boundary_flips}/{len(us) - 1000}")
+    assert boundary_flips <= len(us) - 1000
