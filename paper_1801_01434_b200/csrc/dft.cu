@@ -48,7 +48,13 @@ struct ChunkDesc {
     uint32_t flags;
 };
 
-constexpr int DFT_THREADS = 256;                    // consumer threads (own the outputs)
+#ifndef SHB_DFT_THREADS
+#define SHB_DFT_THREADS 256
+#endif
+#ifndef SHB_DFT_K64
+#define SHB_DFT_K64 4
+#endif
+constexpr int DFT_THREADS = SHB_DFT_THREADS;        // consumer threads (own the outputs)
 constexpr int DFT_CONSUMER_WARPS = DFT_THREADS / 32;
 constexpr int DFT_PRODUCER_THREADS = 32;            // generic path: one TMA producer warp
 constexpr int DFT_STAGES = 4;
@@ -58,7 +64,7 @@ template <typename R>
 struct Prec;
 template <>
 struct Prec<double> {
-    static constexpr int K = 4;            // outputs per thread
+    static constexpr int K = SHB_DFT_K64;  // outputs per thread
     static constexpr uint64_t SEG = 8192;  // terms between exact re-seeds
 };
 template <>
