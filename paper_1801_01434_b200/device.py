@@ -56,11 +56,21 @@ def class_counts(res, ncls: int, out=None):
     return counts
 
 
-def compact_eq(res, k: int, a_begin: int = 0, capacity: int | None = None):
-    """Ascending indices a_begin+i with res[i] == k (device int64 tensor)."""
+def compact_eq(res, k: int, a_begin: int = 0, capacity: int | None = None, expected: int | None = None):
+    """Ascending indices a_begin+i with res[i] == k (device int64 tensor).
+
+    `expected` (the class count, when the caller has it) sizes the output
+    directly and skips the counting probe."""
     t = _t()
     lib = nat.load()
     m = ctypes.c_uint64(0)
+    if expected is not None:
+        sup = t.empty(max(expected, 1), dtype=t.int64, device="cuda")
+        nat.check(lib.shb_compact_eq(_vp(res), res.numel(), k & 0xFFFFFFFF, a_begin, _vp(sup), expected,
+                                     ctypes.byref(m), _stream()), "compact_eq")
+        if int(m.value) != expected:
+            raise RuntimeError(f"compaction found {m.value} indices, class count says {expected}")
+        return sup[:expected]
     cap = res.numel() if capacity is None else capacity
     # count first (cheap) so the output is exactly sized
     probe = t.empty(1, dtype=t.int64, device="cuda")

@@ -168,7 +168,7 @@ def measure_part2(reg: CompositeRegister, s: Sampler) -> tuple[int, CompositeReg
     counts = dev.class_counts(res, ncls_bound).cpu().numpy()
     w0 = uniform_weight(a_unif)
     k = draw_class(counts, w0, s.uniform())
-    support = dev.compact_eq(res, k)
+    support = dev.compact_eq(res, k, expected=int(counts[k]))
     amp = collapsed_amplitude(a_unif, w0, int(support.numel()))
     prog = dev.support_progression(support)
     amps = dev.CollapsedAmplitudes(q, support, amp, prog)
