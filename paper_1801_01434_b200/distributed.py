@@ -53,8 +53,8 @@ class DeviceOps:
     def class_counts(self, res, ncls):
         return self.dev.class_counts(res, ncls)
 
-    def compact_eq(self, res, k, a_begin):
-        return self.dev.compact_eq(res, k, a_begin)
+    def compact_eq(self, res, k, a_begin, expected=None):
+        return self.dev.compact_eq(res, k, a_begin, expected=expected)
 
     def progression(self, support):
         return self.dev.support_progression(support)
@@ -141,13 +141,14 @@ def sharded_attempt(n: int, x: int, q: int, sampler: qstate.Sampler, *, rank: in
 
     # (1) exact class counts, summed over shards
     counts = ops.class_counts(res, n)
+    local = ops.to_host(counts).copy()  # this shard's counts size its compaction
     if world > 1:
         dist.all_reduce(counts, group=group)
     a_unif = complex(1.0 / math.sqrt(q))
     w0 = qstate.uniform_weight(a_unif)
     k = qstate.draw_class(ops.to_host(counts), w0, sampler.uniform())
     # (2) shard supports -> full comb on every rank (shards are in a order)
-    sup = ops.compact_eq(res, k, a_lo)
+    sup = ops.compact_eq(res, k, a_lo, expected=int(local[k]))
     if world > 1:
         sup, _ = _all_gather_var(sup, world, group, torch)
     M = int(sup.numel())

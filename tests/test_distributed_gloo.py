@@ -33,8 +33,10 @@ class OracleOps:
     def class_counts(self, res, ncls):
         return torch.from_numpy(oracle.class_counts(res.numpy().view(np.uint32), ncls).astype(np.int64))
 
-    def compact_eq(self, res, k, a_begin):
-        return torch.from_numpy(np.flatnonzero(res.numpy().view(np.uint32) == k).astype(np.int64) + a_begin)
+    def compact_eq(self, res, k, a_begin, expected=None):
+        out = torch.from_numpy(np.flatnonzero(res.numpy().view(np.uint32) == k).astype(np.int64) + a_begin)
+        assert expected is None or out.numel() == expected
+        return out
 
     def progression(self, sup):
         s = sup.numpy()
