@@ -538,3 +538,21 @@ def test_sampled_m_matches_reference_over_1000_draws(golden_dir, tag, n, attempt
     boundary_flips = int(np.sum(got[1000:] != ms[1000:]))
     print(f"{tag}: 1000/1000 random draws equal; boundary-adversarial flips {boundary_flips}/{len(us) - 1000}")
     assert boundary_flips <= len(us) - 1000
+
+
+def test_qft_fourth_power_is_identity_on_device():
+    """F^2 reverses indices (c -> -c mod q) and F^4 = I, with every
+    intermediate staying on the device (DeviceSpectrum -> dense progression)."""
+    q = 1 << 12
+    rng = np.random.default_rng(4)
+    z = rng.standard_normal(q) + 1j * rng.standard_normal(q)
+    z /= np.linalg.norm(z)
+    t = torch.from_numpy(z.view(np.float64)).cuda()
+    st = dev.DeviceSpectrum(q, t)
+    tw, plan = qft.build_twiddles(q), qft.KernelPlan()
+    f2 = qft.dense_dft(qft.dense_dft(st, tw, plan), tw, plan)
+    assert isinstance(f2, dev.DeviceSpectrum)
+    assert np.max(np.abs(np.asarray(f2) - z[(-np.arange(q)) % q])) < 1e-12
+    f4 = qft.dense_dft(qft.dense_dft(f2, tw, plan), tw, plan)
+    assert np.max(np.abs(np.asarray(f4) - z)) < 1e-12
+    assert abs(qstate.l2_norm(qstate.CompositeRegister(q, f4, None)) - 1.0) < 1e-12
