@@ -556,3 +556,12 @@ def test_qft_fourth_power_is_identity_on_device():
     f4 = qft.dense_dft(qft.dense_dft(f2, tw, plan), tw, plan)
     assert np.max(np.abs(np.asarray(f4) - z)) < 1e-12
     assert abs(qstate.l2_norm(qstate.CompositeRegister(q, f4, None)) - 1.0) < 1e-12
+
+
+def test_c_abi_demo_program(tmp_path):
+    import subprocess
+    from tests.test_abi_and_host import _build_c_demo
+    exe = _build_c_demo(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "row64 = 8" in r.stdout
