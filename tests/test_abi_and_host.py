@@ -102,16 +102,7 @@ def test_abi_argument_errors_without_device(lib):
         nat.check(nat.SHB_ECUDA, "x")
 
 
-def _build_c_demo(tmp_path):
-    import subprocess
-    root = build_mod.PKG.parent
-    exe = tmp_path / "c_abi_demo"
-    cmd = ["gcc", "-O2", "-I", str(root / "include"), str(root / "examples" / "c_abi_demo.c"),
-           "-L", str(build_mod.PKG), f"-Wl,-rpath,{build_mod.PKG}", "-l:libshorb200.so", "-lm", "-o", str(exe)]
-    subprocess.run(cmd, check=True, capture_output=True)
-    return exe
-
-
 def test_c_abi_demo_compiles_and_links(lib, tmp_path):
     # plain C against include/shorb200.h and the .so (running it needs a GPU: test_gpu_parity)
-    assert _build_c_demo(tmp_path).exists()
+    from conftest import build_c_demo
+    assert build_c_demo(tmp_path).exists()

@@ -560,8 +560,8 @@ def test_qft_fourth_power_is_identity_on_device():
 
 def test_c_abi_demo_program(tmp_path):
     import subprocess
-    from tests.test_abi_and_host import _build_c_demo
-    exe = _build_c_demo(tmp_path)
+    from conftest import build_c_demo
+    exe = build_c_demo(tmp_path)
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "row64 = 8" in r.stdout
