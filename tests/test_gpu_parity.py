@@ -441,7 +441,8 @@ def _two_rank_worker(rank, world, port, ret):
         dist.destroy_process_group()
 
 
-def test_sharded_attempt_two_ranks_on_device():
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_attempt_ranks_on_device(world):
     """distributed.sharded_attempt with the real device kernels, 2 ranks on one
     GPU (gloo collectives: host-staged; the kernels never wait on each other).
     Same k, m, support and bitwise-identical spectrum rows as 1 rank."""
@@ -458,13 +459,13 @@ def test_sharded_attempt_two_ranks_on_device():
         port = so.getsockname()[1]
     ctx = mp.get_context("spawn")
     ret = ctx.Manager().dict()
-    procs = [ctx.Process(target=_two_rank_worker, args=(r, 2, port, ret)) for r in range(2)]
+    procs = [ctx.Process(target=_two_rank_worker, args=(r, world, port, ret)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(600)
         assert p.exitcode == 0
-    for r in range(2):
+    for r in range(world):
         g = ret[r]
         assert (g["k"], g["m"], g["M"], g["r"], g["c0"]) == (one.k, one.m, one.M, one.r, one.c0) == \
             (825, 578525, 144631, 116, 29)
