@@ -469,7 +469,7 @@ def test_sharded_attempt_ranks_on_device(world):
         g = ret[r]
         assert (g["k"], g["m"], g["M"], g["r"], g["c0"]) == (one.k, one.m, one.M, one.r, one.c0) == \
             (825, 578525, 144631, 116, 29)
-        ref = full.view(torch.complex128)[torch.tensor(g["rows"], device="cuda")].cpu().numpy().view(np.float64)
+        ref = full.view(torch.complex128)[torch.tensor(g["rows"], dtype=torch.int64, device="cuda")].cpu().numpy().view(np.float64)
         assert np.array_equal(np.asarray(g["vals"]), ref)
 
 
