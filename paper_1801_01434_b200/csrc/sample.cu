@@ -443,11 +443,14 @@ __global__ void __launch_bounds__(SEQ_THREADS, 1)
                             fast = (fl & TR_ALLZERO) != 0;
                             Snew = 0.0;
                         } else {
-                            const int se = ulp_exp(S);
-                            const double u = ldexp(1.0, se);
-                            const uint64_t N = (uint64_t)(S / u) + A;
-                            fast = (se == ue) && !(fl & TR_TIES) && (N < TWO53);
-                            Snew = (double)N * u;
+                            // S > 0 normal: S = sig * 2^(E - 1075) with sig in [2^52, 2^53);
+                            // adding A ulps keeps the exponent while sig + A < 2^53
+                            const uint64_t bits = (uint64_t)__double_as_longlong(S);
+                            const int E = (int)(bits >> 52);
+                            const uint64_t sig = (bits & ((1ull << 52) - 1)) | (1ull << 52);
+                            const uint64_t N = sig + A;
+                            fast = E > 1 && (E - 1075) == ue && !(fl & TR_TIES) && (N < TWO53);
+                            Snew = __longlong_as_double((long long)(((uint64_t)E << 52) | (N - (1ull << 52))));
                         }
                         if (!fast) {
                             stop = tt + i;
