@@ -426,39 +426,50 @@ __global__ void __launch_bounds__(SEQ_THREADS, 1)
     while (t < tile_hi) {
         if (recs != nullptr) {
             if (tid < 32) {
+                // warp 0 advances 32 tile records per step: inside one binade
+                // the running sum after tile i is S + 2^uexp * (A_0 + ... + A_i),
+                // a warp scan; the first tile that crosses a binade, has a tie or
+                // was mispredicted stops the fast walk (ballot).
                 double S = sh.S;
                 uint64_t tt = t, stop = tile_hi;
-                bool slow = false;
-                while (tt < tile_hi && !slow) {
-                    TileRec r{};
-                    if (tt + lane < tile_hi) r = recs[tt + lane];
+                while (tt < tile_hi) {
                     const int cnt = (tile_hi - tt) < 32 ? (int)(tile_hi - tt) : 32;
-                    for (int i = 0; i < cnt; i++) {
-                        const uint64_t A = __shfl_sync(0xffffffffu, r.A, i);
-                        const int ue = __shfl_sync(0xffffffffu, r.uexp, i);
-                        const uint32_t fl = __shfl_sync(0xffffffffu, r.flags, i);
-                        double Snew;
-                        bool fast;
-                        if (S == 0.0) {
-                            fast = (fl & TR_ALLZERO) != 0;
-                            Snew = 0.0;
-                        } else {
-                            // S > 0 normal: S = sig * 2^(E - 1075) with sig in [2^52, 2^53);
-                            // adding A ulps keeps the exponent while sig + A < 2^53
-                            const uint64_t bits = (uint64_t)__double_as_longlong(S);
-                            const int E = (int)(bits >> 52);
-                            const uint64_t sig = (bits & ((1ull << 52) - 1)) | (1ull << 52);
-                            const uint64_t N = sig + A;
-                            fast = E > 1 && (E - 1075) == ue && !(fl & TR_TIES) && (N < TWO53);
-                            Snew = __longlong_as_double((long long)(((uint64_t)E << 52) | (N - (1ull << 52))));
+                    TileRec r{0, 0, TR_ALLZERO};
+                    if (lane < cnt) r = recs[tt + lane];
+                    int first_bad;
+                    if (S == 0.0) {
+                        const bool ok = lane >= cnt || (r.flags & TR_ALLZERO);
+                        const uint32_t bad = ~__ballot_sync(0xffffffffu, ok);
+                        first_bad = bad ? __ffs(bad) - 1 : cnt;
+                        if (mode == 0 && lane < first_bad && lane < cnt) tile_S[tt + lane] = 0.0;
+                    } else {
+                        // S > 0 normal: S = sig * 2^(E - 1075), sig in [2^52, 2^53)
+                        const uint64_t bits = (uint64_t)__double_as_longlong(S);
+                        const int E = (int)(bits >> 52);
+                        const uint64_t sig = (bits & ((1ull << 52) - 1)) | (1ull << 52);
+                        const uint64_t a = lane < cnt ? r.A : 0;
+                        uint64_t P = a;  // inclusive saturating scan of the increments
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint64_t y = __shfl_up_sync(0xffffffffu, P, o);
+                            if (lane >= o) P = sat_add(P, y);
                         }
-                        if (!fast) {
-                            stop = tt + i;
-                            slow = true;
-                            break;
-                        }
-                        if (mode == 0 && lane == 0) tile_S[tt + i] = S;
-                        S = Snew;
+                        const bool ok = lane >= cnt ||
+                                        (E > 1 && (E - 1075) == r.uexp && !(r.flags & TR_TIES) && sig + P < TWO53);
+                        const uint32_t bad = ~__ballot_sync(0xffffffffu, ok);
+                        first_bad = bad ? __ffs(bad) - 1 : cnt;
+                        const uint64_t excl = P - a;  // exact below saturation, which only bad lanes reach
+                        if (mode == 0 && lane < first_bad && lane < cnt)
+                            tile_S[tt + lane] =
+                                __longlong_as_double((long long)(((uint64_t)E << 52) | (sig + excl - (1ull << 52))));
+                        // running sum after the last good tile
+                        const uint64_t Pl = __shfl_sync(0xffffffffu, P, first_bad > 0 ? first_bad - 1 : 0);
+                        if (first_bad > 0)
+                            S = __longlong_as_double((long long)(((uint64_t)E << 52) | (sig + Pl - (1ull << 52))));
+                    }
+                    if (first_bad < cnt) {
+                        stop = tt + first_bad;
+                        break;
                     }
                     tt += cnt;
                 }
