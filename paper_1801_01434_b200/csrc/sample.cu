@@ -432,10 +432,12 @@ __global__ void __launch_bounds__(SEQ_THREADS, 1)
                 // was mispredicted stops the fast walk (ballot).
                 double S = sh.S;
                 uint64_t tt = t, stop = tile_hi;
+                TileRec rn{0, 0, TR_ALLZERO};  // records of the next step, loaded one step ahead
+                if (tt + lane < tile_hi) rn = recs[tt + lane];
                 while (tt < tile_hi) {
                     const int cnt = (tile_hi - tt) < 32 ? (int)(tile_hi - tt) : 32;
-                    TileRec r{0, 0, TR_ALLZERO};
-                    if (lane < cnt) r = recs[tt + lane];
+                    const TileRec r = rn;
+                    if (tt + 32 + lane < tile_hi) rn = recs[tt + 32 + lane];
                     int first_bad;
                     if (S == 0.0) {
                         const bool ok = lane >= cnt || (r.flags & TR_ALLZERO);
