@@ -123,12 +123,11 @@ def _class_probabilities(counts: np.ndarray, w0: float) -> np.ndarray:
     sequential float64 sum of counts[v] copies of w0.
     """
     out = np.zeros(counts.size, dtype=np.float64)
-    memo: dict[int, float] = {}
-    for v in np.flatnonzero(counts):
-        c = int(counts[v])
-        if c not in memo:
-            memo[c] = nat.host_seqsum_const(w0, c)
-        out[v] = memo[c]
+    nz = np.flatnonzero(counts)
+    # the sum depends only on the count: one closed-form evaluation per distinct count
+    uniq, inv = np.unique(np.asarray(counts)[nz], return_inverse=True)
+    vals = np.array([nat.host_seqsum_const(w0, int(c)) for c in uniq], dtype=np.float64)
+    out[nz] = vals[inv]
     return out
 
 
