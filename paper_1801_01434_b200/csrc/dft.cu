@@ -34,6 +34,7 @@
 // The epilogue fuses |V|^2 (hypot^2, as np.abs(.)**2, qstate.py:141) and a
 // deterministic per-CTA sum of it (norm check, qstate.py:50-53).
 #include <math.h>
+#include <stdlib.h>
 #include <vector>
 
 #include "shb_internal.cuh"
@@ -367,6 +368,252 @@ static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t s
                      : launch_dft_t<R, UNIF, false>(a, length, tiles, st);
 }
 
+
+// ---------------------------------------------------------------------------
+// FP64 tensor-core (DMMA) formulation of the same sum.  With j = (jb*8 + j1)*B + k
+// (B = MMA_B, j1 < 8, k < B):
+//   sum_j a_j w^j = sum_jb w^{8B jb} sum_j1 w^{B j1} T_jb[j1, c],
+//   T_jb[j1, c] = sum_k a_{(jb*8+j1)*B+k} * w_c^k
+// T_jb is an [8 x B] x [B x 8] GEMM per 8 outputs: mma.sync m8n8k4 f64, four
+// real DMMAs per complex product (8 flops per phase term, as the vector
+// kernels).  A = amplitudes (row j1, col k), B = G[k][c] = w_c^k (exact,
+// sincospi), D[j1][c] = T.  Each lane keeps a Horner over blocks for its two
+// D columns (U = w^{-8B}); every MMA_SEG_BLOCKS blocks the lane's partial is
+// multiplied by the exact seed e^{i theta(a0 + (8B jb_last + B j1) stride, c)}
+// and added to its total; one cross-lane reduction at the end.
+// m8n8k4.f64 fragments: A[r = lane/4][k = lane%4], B[k = lane%4][n = lane/4],
+// C/D[r = lane/4][n = 2*(lane%4) + {0,1}].
+constexpr int MMA_B = 32;                  // k extent per block row
+constexpr int MMA_KS = MMA_B / 4;          // k-steps of 4
+constexpr int MMA_BLOCK = 8 * MMA_B;       // amplitudes per block (256)
+constexpr int MMA_CT = 2;                  // 8-output tiles per warp
+constexpr int MMA_WARPS = 8;               // consumer warps
+constexpr int MMA_OUT_PER_CTA = MMA_WARPS * MMA_CT * 8;  // 128
+constexpr int MMA_SEG_BLOCKS = 32;         // exact re-seed every 8192 amplitudes
+constexpr int MMA_CHUNK = 1024;            // amplitudes per smem stage (4 blocks)
+
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+struct MmaArgs {
+    const double2 *amps;  // null on the uniform path
+    uint64_t length;       // progression length (amplitudes)
+    uint64_t a0, stride, q;
+    double two_over_q;
+    uint64_t c_begin, c_count;
+    double amp_re, amp_im;  // uniform amplitude (uniform path)
+    double out_re, out_im;  // output factor
+    double2 *out;
+    double *prob;
+    double *block_sums;
+};
+
+template <bool UNIF>
+__global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1)
+    dft_mma_kernel(const MmaArgs p)
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double2 *buf = reinterpret_cast<double2 *>(smem_raw);
+    __shared__ __align__(8) uint64_t full_bar[DFT_STAGES];
+    __shared__ __align__(8) uint64_t empty_bar[DFT_STAGES];
+    __shared__ double red_tmp[MMA_WARPS];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t q = p.q, qmask = q - 1;
+    const uint64_t nblocks = (p.length + MMA_BLOCK - 1) / MMA_BLOCK;
+    const uint64_t nchunks = (p.length + MMA_CHUNK - 1) / MMA_CHUNK;
+    const uint64_t cta_c = (uint64_t)blockIdx.x * MMA_OUT_PER_CTA;
+    const bool consumer = UNIF || warp < MMA_WARPS;
+
+    if (!UNIF) {
+        if (tid == 0) {
+#pragma unroll
+            for (int s = 0; s < DFT_STAGES; s++) {
+                mbar_init(&full_bar[s], 1);
+                mbar_init(&empty_bar[s], MMA_WARPS);
+            }
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (tid == MMA_WARPS * 32) {  // TMA producer
+            for (uint64_t ch = 0; ch < nchunks; ch++) {
+                const int s = (int)(ch % DFT_STAGES);
+                if (ch >= DFT_STAGES) mbar_wait(&empty_bar[s], (uint32_t)((ch / DFT_STAGES) - 1) & 1u);
+                const uint64_t j0 = ch * MMA_CHUNK;
+                const uint64_t cnt = (p.length - j0) < MMA_CHUNK ? (p.length - j0) : MMA_CHUNK;
+                mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(cnt * 16));
+                tma_bulk_g2s(buf + (size_t)s * MMA_CHUNK, p.amps + j0, (uint32_t)(cnt * 16), &full_bar[s]);
+            }
+        }
+    }
+
+    // this lane's outputs: B-fragment column (G) and D-fragment columns
+    const int r = lane >> 2, kq = lane & 3;
+    uint64_t cG[MMA_CT], cD[MMA_CT][2];
+    double gr[MMA_CT][MMA_KS], gi[MMA_CT][MMA_KS];
+    double ur[MMA_CT][2], ui[MMA_CT][2];       // U = w^{-8B} for the D columns
+    double hr[MMA_CT][2], hi[MMA_CT][2];       // per-lane Horner over blocks (this segment)
+    double vr[MMA_CT][2], vi[MMA_CT][2];       // per-lane totals
+    double dr[MMA_CT][2], di[MMA_CT][2];       // MMA accumulators (Re T, Im T)
+#pragma unroll
+    for (int ct = 0; ct < MMA_CT; ct++) {
+        const uint64_t tile = cta_c + (uint64_t)warp * (MMA_CT * 8) + ct * 8;
+        cG[ct] = p.c_begin + tile + r;
+#pragma unroll
+        for (int ks = 0; ks < MMA_KS; ks++) {
+            const uint64_t k = (uint64_t)ks * 4 + kq;
+            double co, si;
+            phase((k * p.stride * cG[ct]) & qmask, q, p.two_over_q, co, si);
+            gr[ct][ks] = co;
+            gi[ct][ks] = si;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            cD[ct][h] = p.c_begin + tile + 2 * kq + h;
+            double co, si;
+            phase(((uint64_t)MMA_BLOCK * p.stride * cD[ct][h]) & qmask, q, p.two_over_q, co, si);
+            ur[ct][h] = co;
+            ui[ct][h] = -si;  // w^{-8B}
+            hr[ct][h] = hi[ct][h] = vr[ct][h] = vi[ct][h] = 0.0;
+            dr[ct][h] = di[ct][h] = 0.0;
+        }
+    }
+
+    uint64_t seg_blocks = 0;
+    for (uint64_t jb = 0; consumer && jb < nblocks; jb++) {
+        const uint64_t ch = jb / (MMA_CHUNK / MMA_BLOCK);
+        const int s = (int)(ch % DFT_STAGES);
+        const int boff = (int)(jb % (MMA_CHUNK / MMA_BLOCK)) * MMA_BLOCK;
+        if (!UNIF && boff == 0) mbar_wait(&full_bar[s], (uint32_t)(ch / DFT_STAGES) & 1u);
+        const double2 *sb = buf + (size_t)s * MMA_CHUNK + boff;
+        const uint64_t jblk = jb * MMA_BLOCK;
+#pragma unroll
+        for (int ks = 0; ks < MMA_KS; ks++) {
+            const int jl = r * MMA_B + ks * 4 + kq;  // A fragment: row j1 = r, col k
+            double ar, ai;
+            if (jblk + jl < p.length) {
+                if (UNIF) {
+                    ar = p.amp_re;
+                    ai = p.amp_im;
+                } else {
+                    const double2 av = sb[jl];
+                    ar = av.x;
+                    ai = av.y;
+                }
+            } else {
+                ar = ai = 0.0;  // ragged tail
+            }
+#pragma unroll
+            for (int ct = 0; ct < MMA_CT; ct++) {
+                // T = A * G (complex): Re += ar*gr - ai*gi ; Im += ar*gi + ai*gr
+                dmma_8x8x4(dr[ct][0], dr[ct][1], ar, gr[ct][ks]);
+                dmma_8x8x4(dr[ct][0], dr[ct][1], -ai, gi[ct][ks]);
+                dmma_8x8x4(di[ct][0], di[ct][1], ar, gi[ct][ks]);
+                dmma_8x8x4(di[ct][0], di[ct][1], ai, gr[ct][ks]);
+            }
+        }
+        if (!UNIF && (boff + MMA_BLOCK == MMA_CHUNK || jb + 1 == nblocks)) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[s]);
+        }
+        // Horner over blocks: h = h * w^{-8B} + T ; T reset
+#pragma unroll
+        for (int ct = 0; ct < MMA_CT; ct++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const double nr = fma(hr[ct][h], ur[ct][h], fma(-hi[ct][h], ui[ct][h], dr[ct][h]));
+                const double ni = fma(hr[ct][h], ui[ct][h], fma(hi[ct][h], ur[ct][h], di[ct][h]));
+                hr[ct][h] = nr;
+                hi[ct][h] = ni;
+                dr[ct][h] = di[ct][h] = 0.0;
+            }
+        if (++seg_blocks == MMA_SEG_BLOCKS || jb + 1 == nblocks) {
+            // exact seed of this lane's last row: a0 + (8B jb + B r) * stride
+            const uint64_t a_lane = p.a0 + (jb * MMA_BLOCK + (uint64_t)r * MMA_B) * p.stride;
+#pragma unroll
+            for (int ct = 0; ct < MMA_CT; ct++)
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    double sc, ss;
+                    phase((a_lane * cD[ct][h]) & qmask, q, p.two_over_q, sc, ss);
+                    vr[ct][h] = fma(sc, hr[ct][h], fma(-ss, hi[ct][h], vr[ct][h]));
+                    vi[ct][h] = fma(sc, hi[ct][h], fma(ss, hr[ct][h], vi[ct][h]));
+                    hr[ct][h] = hi[ct][h] = 0.0;
+                }
+            seg_blocks = 0;
+        }
+    }
+
+    // cross-lane sum over the 8 rows (lanes with equal lane%4), then lanes 0..3 write
+    double psum = 0.0;
+    if (consumer) {
+#pragma unroll
+        for (int ct = 0; ct < MMA_CT; ct++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1) {
+                    vr[ct][h] += __shfl_xor_sync(0xffffffffu, vr[ct][h], o);
+                    vi[ct][h] += __shfl_xor_sync(0xffffffffu, vi[ct][h], o);
+                }
+                const uint64_t ci = cD[ct][h] - p.c_begin;
+                if (r == 0 && ci < p.c_count) {
+                    const double o_re = vr[ct][h] * p.out_re - vi[ct][h] * p.out_im;
+                    const double o_im = vr[ct][h] * p.out_im + vi[ct][h] * p.out_re;
+                    p.out[ci] = make_double2(o_re, o_im);
+                    const double hh = hypot(o_re, o_im);
+                    const double pr = hh * hh;
+                    if (p.prob) p.prob[ci] = pr;
+                    psum += pr;
+                }
+            }
+    }
+    if (p.block_sums) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) psum += __shfl_down_sync(0xffffffffu, psum, o);
+        if (lane == 0 && consumer) red_tmp[warp] = psum;
+        __syncthreads();
+        if (tid == 0) {
+            double b = 0.0;
+#pragma unroll
+            for (int w = 0; w < MMA_WARPS; w++) b += red_tmp[w];
+            p.block_sums[blockIdx.x] = b;
+        }
+    }
+}
+
+template <bool UNIF>
+static int launch_dft_mma(const MmaArgs &a, cudaStream_t st)
+{
+    const size_t smem = UNIF ? 0 : (size_t)DFT_STAGES * MMA_CHUNK * sizeof(double2);
+    static bool attr_done = false;
+    if (!attr_done && smem) {
+        SHB_TRY_CUDA(cudaFuncSetAttribute(dft_mma_kernel<UNIF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        attr_done = true;
+    }
+    const uint64_t nblk = (a.c_count + MMA_OUT_PER_CTA - 1) / MMA_OUT_PER_CTA;
+    if (nblk > 0x7FFFFFFFull) return set_error(SHB_EINVAL, "too many outputs for one launch");
+    const unsigned nthreads = UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32;
+    dft_mma_kernel<UNIF><<<(unsigned)nblk, nthreads, smem, st>>>(a);
+    SHB_LAUNCHED();
+    SHB_TRY_CUDA(cudaGetLastError());
+    return SHB_OK;
+}
+
+// engine choice for FP64, tiles == 1: "mma" (DMMA GEMM form) or "vector";
+// SHB_DFT_ENGINE overrides for testing both
+static bool use_mma_engine(bool uniform)
+{
+    const char *e = getenv("SHB_DFT_ENGINE");
+    if (e && e[0]) return e[0] == 'm';
+    return !uniform;  // default: tensor-core path for general amplitudes
+}
+
 static int validate(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin,
                     uint64_t c_count, uint32_t tiles, int precision, double *d_out)
 {
@@ -423,6 +670,11 @@ extern "C" int shb_dft(const double *d_amps, uint64_t length, uint64_t a0, uint6
     a.out_im = 0.0;
     cudaStream_t st = as_stream(stream);
     if (precision == SHB_FP32) return launch_dft<float, false>(a, length, tiles, st);
+    if (tiles == 1 && length && use_mma_engine(false)) {
+        MmaArgs m{(const double2 *)d_amps, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
+                  0.0, 0.0, scale, 0.0, (double2 *)d_out, d_prob, d_block_sums};
+        return launch_dft_mma<false>(m, st);
+    }
     return launch_dft<double, false>(a, length, tiles, st);
 }
 
@@ -438,5 +690,11 @@ extern "C" int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, ui
     a.out_im = amp_im * scale;
     cudaStream_t st = as_stream(stream);
     if (precision == SHB_FP32) return launch_dft<float, true>(a, length, tiles, st);
+    if (tiles == 1 && length && use_mma_engine(true)) {
+        // the amplitude is factored out (out factor = amp*scale): the MMA runs on ones
+        MmaArgs m{nullptr, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
+                  1.0, 0.0, a.out_re, a.out_im, (double2 *)d_out, d_prob, d_block_sums};
+        return launch_dft_mma<true>(m, st);
+    }
     return launch_dft<double, true>(a, length, tiles, st);
 }
