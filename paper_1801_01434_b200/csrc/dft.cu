@@ -458,7 +458,9 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1
     double ur[MMA_CT][2], ui[MMA_CT][2];       // U = w^{-8B} for the D columns
     double hr[MMA_CT][2], hi[MMA_CT][2];       // per-lane Horner over blocks (this segment)
     double vr[MMA_CT][2], vi[MMA_CT][2];       // per-lane totals
-    double dr[MMA_CT][2], di[MMA_CT][2];       // MMA accumulators (Re T, Im T)
+    // four independent MMA accumulators per tile (Re T = rr + ii, Im T = ri + ir)
+    // so consecutive DMMAs never wait on each other within a k-step
+    double drr[MMA_CT][2], dii[MMA_CT][2], dri[MMA_CT][2], dir_[MMA_CT][2];
 #pragma unroll
     for (int ct = 0; ct < MMA_CT; ct++) {
         const uint64_t tile = cta_c + (uint64_t)warp * (MMA_CT * 8) + ct * 8;
@@ -479,7 +481,7 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1
             ur[ct][h] = co;
             ui[ct][h] = -si;  // w^{-8B}
             hr[ct][h] = hi[ct][h] = vr[ct][h] = vi[ct][h] = 0.0;
-            dr[ct][h] = di[ct][h] = 0.0;
+            drr[ct][h] = dii[ct][h] = dri[ct][h] = dir_[ct][h] = 0.0;
         }
     }
 
@@ -510,10 +512,10 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1
 #pragma unroll
             for (int ct = 0; ct < MMA_CT; ct++) {
                 // T = A * G (complex): Re += ar*gr - ai*gi ; Im += ar*gi + ai*gr
-                dmma_8x8x4(dr[ct][0], dr[ct][1], ar, gr[ct][ks]);
-                dmma_8x8x4(dr[ct][0], dr[ct][1], -ai, gi[ct][ks]);
-                dmma_8x8x4(di[ct][0], di[ct][1], ar, gi[ct][ks]);
-                dmma_8x8x4(di[ct][0], di[ct][1], ai, gr[ct][ks]);
+                dmma_8x8x4(drr[ct][0], drr[ct][1], ar, gr[ct][ks]);
+                dmma_8x8x4(dii[ct][0], dii[ct][1], -ai, gi[ct][ks]);
+                dmma_8x8x4(dri[ct][0], dri[ct][1], ar, gi[ct][ks]);
+                dmma_8x8x4(dir_[ct][0], dir_[ct][1], ai, gr[ct][ks]);
             }
         }
         if (!UNIF && (boff + MMA_BLOCK == MMA_CHUNK || jb + 1 == nblocks)) {
@@ -525,11 +527,12 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1
         for (int ct = 0; ct < MMA_CT; ct++)
 #pragma unroll
             for (int h = 0; h < 2; h++) {
-                const double nr = fma(hr[ct][h], ur[ct][h], fma(-hi[ct][h], ui[ct][h], dr[ct][h]));
-                const double ni = fma(hr[ct][h], ui[ct][h], fma(hi[ct][h], ur[ct][h], di[ct][h]));
+                const double tre = drr[ct][h] + dii[ct][h], tim = dri[ct][h] + dir_[ct][h];
+                const double nr = fma(hr[ct][h], ur[ct][h], fma(-hi[ct][h], ui[ct][h], tre));
+                const double ni = fma(hr[ct][h], ui[ct][h], fma(hi[ct][h], ur[ct][h], tim));
                 hr[ct][h] = nr;
                 hi[ct][h] = ni;
-                dr[ct][h] = di[ct][h] = 0.0;
+                drr[ct][h] = dii[ct][h] = dri[ct][h] = dir_[ct][h] = 0.0;
             }
         if (++seg_blocks == MMA_SEG_BLOCKS || jb + 1 == nblocks) {
             // exact seed of this lane's last row: a0 + (8B jb + B r) * stride
@@ -586,8 +589,24 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1
     }
 }
 
+// Fold MMA per-CTA |V|^2 sums (128 outputs each) into the vector-kernel layout
+// the caller allocated (shb_dft_num_blocks: DFT_THREADS*K outputs per slot), in
+// a fixed order so the norm stays deterministic.
+__global__ void group_sums_kernel(const double *__restrict__ part, uint64_t nparts, int group,
+                                  double *__restrict__ out, uint64_t nout)
+{
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nout) return;
+    double s = 0.0;
+    for (int i = 0; i < group; i++) {
+        const uint64_t j = g * group + i;
+        if (j < nparts) s += part[j];
+    }
+    out[g] = s;
+}
+
 template <bool UNIF>
-static int launch_dft_mma(const MmaArgs &a, cudaStream_t st)
+static int launch_dft_mma(MmaArgs a, cudaStream_t st)
 {
     const size_t smem = UNIF ? 0 : (size_t)DFT_STAGES * MMA_CHUNK * sizeof(double2);
     static bool attr_done = false;
@@ -599,8 +618,22 @@ static int launch_dft_mma(const MmaArgs &a, cudaStream_t st)
     const uint64_t nblk = (a.c_count + MMA_OUT_PER_CTA - 1) / MMA_OUT_PER_CTA;
     if (nblk > 0x7FFFFFFFull) return set_error(SHB_EINVAL, "too many outputs for one launch");
     const unsigned nthreads = UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32;
+    double *caller_sums = a.block_sums;
+    Scratch part;
+    if (caller_sums) {
+        SHB_TRY(scratch_alloc(part, sizeof(double) * nblk, st));
+        a.block_sums = (double *)part.ptr;
+    }
     dft_mma_kernel<UNIF><<<(unsigned)nblk, nthreads, smem, st>>>(a);
     SHB_LAUNCHED();
+    if (caller_sums) {
+        constexpr int group = DFT_THREADS * Prec<double>::K / MMA_OUT_PER_CTA;
+        static_assert(group * MMA_OUT_PER_CTA == DFT_THREADS * Prec<double>::K, "slot sizes must nest");
+        const uint64_t nout = (a.c_count + DFT_THREADS * Prec<double>::K - 1) / (DFT_THREADS * Prec<double>::K);
+        group_sums_kernel<<<(unsigned)((nout + 255) / 256), 256, 0, st>>>((const double *)part.ptr, nblk, group,
+                                                                          caller_sums, nout);
+        SHB_LAUNCHED();
+    }
     SHB_TRY_CUDA(cudaGetLastError());
     return SHB_OK;
 }
