@@ -458,9 +458,7 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1
     double ur[MMA_CT][2], ui[MMA_CT][2];       // U = w^{-8B} for the D columns
     double hr[MMA_CT][2], hi[MMA_CT][2];       // per-lane Horner over blocks (this segment)
     double vr[MMA_CT][2], vi[MMA_CT][2];       // per-lane totals
-    // four independent MMA accumulators per tile (Re T = rr + ii, Im T = ri + ir)
-    // so consecutive DMMAs never wait on each other within a k-step
-    double drr[MMA_CT][2], dii[MMA_CT][2], dri[MMA_CT][2], dir_[MMA_CT][2];
+    double dr[MMA_CT][2], di[MMA_CT][2];       // MMA accumulators (Re T, Im T)
 #pragma unroll
     for (int ct = 0; ct < MMA_CT; ct++) {
         const uint64_t tile = cta_c + (uint64_t)warp * (MMA_CT * 8) + ct * 8;
@@ -481,7 +479,7 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1
             ur[ct][h] = co;
             ui[ct][h] = -si;  // w^{-8B}
             hr[ct][h] = hi[ct][h] = vr[ct][h] = vi[ct][h] = 0.0;
-            drr[ct][h] = dii[ct][h] = dri[ct][h] = dir_[ct][h] = 0.0;
+            dr[ct][h] = di[ct][h] = 0.0;
         }
     }
 
@@ -512,10 +510,10 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1
 #pragma unroll
             for (int ct = 0; ct < MMA_CT; ct++) {
                 // T = A * G (complex): Re += ar*gr - ai*gi ; Im += ar*gi + ai*gr
-                dmma_8x8x4(drr[ct][0], drr[ct][1], ar, gr[ct][ks]);
-                dmma_8x8x4(dii[ct][0], dii[ct][1], -ai, gi[ct][ks]);
-                dmma_8x8x4(dri[ct][0], dri[ct][1], ar, gi[ct][ks]);
-                dmma_8x8x4(dir_[ct][0], dir_[ct][1], ai, gr[ct][ks]);
+                dmma_8x8x4(dr[ct][0], dr[ct][1], ar, gr[ct][ks]);
+                dmma_8x8x4(dr[ct][0], dr[ct][1], -ai, gi[ct][ks]);
+                dmma_8x8x4(di[ct][0], di[ct][1], ar, gi[ct][ks]);
+                dmma_8x8x4(di[ct][0], di[ct][1], ai, gr[ct][ks]);
             }
         }
         if (!UNIF && (boff + MMA_BLOCK == MMA_CHUNK || jb + 1 == nblocks)) {
@@ -527,12 +525,11 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1
         for (int ct = 0; ct < MMA_CT; ct++)
 #pragma unroll
             for (int h = 0; h < 2; h++) {
-                const double tre = drr[ct][h] + dii[ct][h], tim = dri[ct][h] + dir_[ct][h];
-                const double nr = fma(hr[ct][h], ur[ct][h], fma(-hi[ct][h], ui[ct][h], tre));
-                const double ni = fma(hr[ct][h], ui[ct][h], fma(hi[ct][h], ur[ct][h], tim));
+                const double nr = fma(hr[ct][h], ur[ct][h], fma(-hi[ct][h], ui[ct][h], dr[ct][h]));
+                const double ni = fma(hr[ct][h], ui[ct][h], fma(hi[ct][h], ur[ct][h], di[ct][h]));
                 hr[ct][h] = nr;
                 hi[ct][h] = ni;
-                drr[ct][h] = dii[ct][h] = dri[ct][h] = dir_[ct][h] = 0.0;
+                dr[ct][h] = di[ct][h] = 0.0;
             }
         if (++seg_blocks == MMA_SEG_BLOCKS || jb + 1 == nblocks) {
             // exact seed of this lane's last row: a0 + (8B jb + B r) * stride

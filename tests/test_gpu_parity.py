@@ -566,3 +566,25 @@ def test_c_abi_demo_program(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "row64 = 8" in r.stdout
+
+
+@pytest.mark.parametrize("engine", ["vector", "mma"])
+def test_both_fp64_engines_vs_oracle(engine, monkeypatch):
+    """The FP64 DFT has two kernels for tiles == 1: the vector Horner kernel and
+    the DMMA (FP64 tensor-core) GEMM-factored kernel.  Both against the oracle on
+    ragged sizes, output shards and the uniform / generic amplitude paths."""
+    monkeypatch.setenv("SHB_DFT_ENGINE", engine)
+    rng = np.random.default_rng(21)
+    for q, c0, r, M in [(1 << 10, 5, 3, 1), (1 << 10, 5, 3, 255), (1 << 12, 1, 7, 585), (1 << 16, 11, 12, 5461)]:
+        supp = c0 + r * np.arange(M, dtype=np.uint64)
+        amps_h = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+        amps = torch.from_numpy(amps_h.view(np.float64)).cuda()
+        for lo, cnt in [(0, q), (77, 129), (q - 130, 130)]:
+            rows = np.arange(lo, lo + cnt, dtype=np.uint64)
+            out, prob, bs = dev.dft(amps, M, c0, r, q, lo, cnt)
+            ref = oracle.dft_rows(supp, amps_h, q, rows)
+            assert np.max(np.abs(out.cpu().numpy().view(np.complex128) - ref)) < 1e-12 * max(1, np.abs(ref).max())
+            assert abs(dev.dsum(bs) - float(prob.sum())) <= 1e-9 * float(prob.sum())
+            ou, pu, bu = dev.dft_uniform(0.3 - 0.1j, M, c0, r, q, lo, cnt)
+            refu = oracle.dft_rows(supp, np.full(M, 0.3 - 0.1j), q, rows)
+            assert np.max(np.abs(ou.cpu().numpy().view(np.complex128) - refu)) < 1e-12 * max(1, np.abs(refu).max())
