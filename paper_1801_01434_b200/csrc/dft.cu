@@ -635,13 +635,19 @@ static int launch_dft_mma(MmaArgs a, cudaStream_t st)
     return SHB_OK;
 }
 
-// engine choice for FP64, tiles == 1: "mma" (DMMA GEMM form) or "vector";
-// SHB_DFT_ENGINE overrides for testing both
-static bool use_mma_engine(bool uniform)
+// Engine choice for FP64, tiles == 1 (measured, profiles/r01_mma_vs_vector.json):
+// * general amplitudes: the DMMA GEMM form (27.7 vs 26.0 TF at q = 2^24; the
+//   vector form is register-file bound there);
+// * uniform comb: the vector Horner kernel (34.4 vs 32.6 TF at 2^24), except
+//   for small output ranges that its 1024-output CTAs cannot spread over 148 SMs
+//   (q = 2^16: 18.9 vs 12.1 TF) -- the DMMA form has 128 outputs per CTA.
+// SHB_DFT_ENGINE=vector|mma overrides (tests run both).
+static bool use_mma_engine(bool uniform, uint64_t c_count)
 {
     const char *e = getenv("SHB_DFT_ENGINE");
     if (e && e[0]) return e[0] == 'm';
-    return !uniform;  // default: tensor-core path for general amplitudes
+    if (!uniform) return true;
+    return c_count < (uint64_t)sm_count() * 2 * DFT_THREADS * Prec<double>::K * 4;
 }
 
 static int validate(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin,
@@ -700,7 +706,7 @@ extern "C" int shb_dft(const double *d_amps, uint64_t length, uint64_t a0, uint6
     a.out_im = 0.0;
     cudaStream_t st = as_stream(stream);
     if (precision == SHB_FP32) return launch_dft<float, false>(a, length, tiles, st);
-    if (tiles == 1 && length && use_mma_engine(false)) {
+    if (tiles == 1 && length && use_mma_engine(false, c_count)) {
         MmaArgs m{(const double2 *)d_amps, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
                   0.0, 0.0, scale, 0.0, (double2 *)d_out, d_prob, d_block_sums};
         return launch_dft_mma<false>(m, st);
@@ -720,7 +726,7 @@ extern "C" int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, ui
     a.out_im = amp_im * scale;
     cudaStream_t st = as_stream(stream);
     if (precision == SHB_FP32) return launch_dft<float, true>(a, length, tiles, st);
-    if (tiles == 1 && length && use_mma_engine(true)) {
+    if (tiles == 1 && length && use_mma_engine(true, c_count)) {
         // the amplitude is factored out (out factor = amp*scale): the MMA runs on ones
         MmaArgs m{nullptr, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
                   1.0, 0.0, a.out_re, a.out_im, (double2 *)d_out, d_prob, d_block_sums};
