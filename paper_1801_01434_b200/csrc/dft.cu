@@ -642,12 +642,15 @@ static int launch_dft_mma(MmaArgs a, cudaStream_t st)
 //   for small output ranges that its 1024-output CTAs cannot spread over 148 SMs
 //   (q = 2^16: 18.9 vs 12.1 TF) -- the DMMA form has 128 outputs per CTA.
 // SHB_DFT_ENGINE=vector|mma overrides (tests run both).
-static bool use_mma_engine(bool uniform, uint64_t c_count)
+// The choice depends on q only (not on this launch's output range), so every
+// output shard of a transform uses the same kernel and the spectrum stays
+// bitwise identical for any number of ranks.
+static bool use_mma_engine(bool uniform, uint64_t q)
 {
     const char *e = getenv("SHB_DFT_ENGINE");
     if (e && e[0]) return e[0] == 'm';
     if (!uniform) return true;
-    return c_count < (uint64_t)sm_count() * 2 * DFT_THREADS * Prec<double>::K * 4;
+    return q < (1ull << 21);  // below ~1.2M outputs the vector CTAs cannot fill 148 SMs
 }
 
 static int validate(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin,
@@ -706,7 +709,7 @@ extern "C" int shb_dft(const double *d_amps, uint64_t length, uint64_t a0, uint6
     a.out_im = 0.0;
     cudaStream_t st = as_stream(stream);
     if (precision == SHB_FP32) return launch_dft<float, false>(a, length, tiles, st);
-    if (tiles == 1 && length && use_mma_engine(false, c_count)) {
+    if (tiles == 1 && length && use_mma_engine(false, q)) {
         MmaArgs m{(const double2 *)d_amps, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
                   0.0, 0.0, scale, 0.0, (double2 *)d_out, d_prob, d_block_sums};
         return launch_dft_mma<false>(m, st);
@@ -726,7 +729,7 @@ extern "C" int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, ui
     a.out_im = amp_im * scale;
     cudaStream_t st = as_stream(stream);
     if (precision == SHB_FP32) return launch_dft<float, true>(a, length, tiles, st);
-    if (tiles == 1 && length && use_mma_engine(true, c_count)) {
+    if (tiles == 1 && length && use_mma_engine(true, q)) {
         // the amplitude is factored out (out factor = amp*scale): the MMA runs on ones
         MmaArgs m{nullptr, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
                   1.0, 0.0, a.out_re, a.out_im, (double2 *)d_out, d_prob, d_block_sums};

@@ -233,9 +233,12 @@ def test_spec_qft_examples():
         qft.dense_dft(u, qft.build_twiddles(256), qft.KernelPlan(tiles=2))
 
 
-def test_dft_sharded_rows_bitwise_identical():
-    # output sharding must not change any value (multi-GPU bitwise requirement)
-    q, c0, r, M = 1 << 18, 11, 12, ((1 << 18) - 1 - 11) // 12 + 1
+@pytest.mark.parametrize("q", [1 << 18, 1 << 21])
+def test_dft_sharded_rows_bitwise_identical(q):
+    # output sharding must not change any value (multi-GPU bitwise requirement),
+    # including across the engine-selection threshold of the uniform path
+    c0, r = 11, 12
+    M = (q - 1 - c0) // r + 1
     sup = torch.arange(M, dtype=torch.int64, device="cuda") * r + c0
     amps = dev.fill_progression(sup, M, c0, r, M, complex(1 / math.sqrt(M)))
     for fn in (lambda lo, cnt: dev.dft(amps, M, c0, r, q, lo, cnt)[0],
