@@ -383,13 +383,19 @@ static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t s
 // and added to its total; one cross-lane reduction at the end.
 // m8n8k4.f64 fragments: A[r = lane/4][k = lane%4], B[k = lane%4][n = lane/4],
 // C/D[r = lane/4][n = 2*(lane%4) + {0,1}].
-constexpr int MMA_B = 32;                  // k extent per block row
+#ifndef SHB_MMA_B
+#define SHB_MMA_B 32
+#endif
+#ifndef SHB_MMA_CT
+#define SHB_MMA_CT 2
+#endif
+constexpr int MMA_B = SHB_MMA_B;           // k extent per block row
 constexpr int MMA_KS = MMA_B / 4;          // k-steps of 4
 constexpr int MMA_BLOCK = 8 * MMA_B;       // amplitudes per block (256)
-constexpr int MMA_CT = 2;                  // 8-output tiles per warp
+constexpr int MMA_CT = SHB_MMA_CT;         // 8-output tiles per warp
 constexpr int MMA_WARPS = 8;               // consumer warps
 constexpr int MMA_OUT_PER_CTA = MMA_WARPS * MMA_CT * 8;  // 128
-constexpr int MMA_SEG_BLOCKS = 32;         // exact re-seed every 8192 amplitudes
+constexpr int MMA_SEG_BLOCKS = 8192 / MMA_BLOCK;  // exact re-seed every 8192 amplitudes
 constexpr int MMA_CHUNK = 1024;            // amplitudes per smem stage (4 blocks)
 
 __device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b)

@@ -1,6 +1,7 @@
 """Time DFT kernel shape variants (scripts/build_variants.sh) at q = 2^24 on the
 n=3127 comb: generic (random complex amplitudes) and uniform, FP64."""
 import json
+import os
 import math
 import sys
 from pathlib import Path
@@ -11,6 +12,9 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1801_01434_b200 import _native as nat  # noqa: E402
+
+if len(sys.argv) > 1:
+    os.environ["SHB_DFT_ENGINE"] = sys.argv[1]
 from paper_1801_01434_b200 import device as dev  # noqa: E402
 
 q, c0, r, M = 1 << 24, 29, 116, 144631
