@@ -344,12 +344,9 @@ static int launch_dft_t(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t
                                      cudaMemcpyHostToDevice, st));
     a.sched = (const ChunkDesc *)d_sched.ptr;
     const size_t smem = UNIF ? 0 : (size_t)DFT_STAGES * DFT_CHUNK * sizeof(double2);
-    static bool attr_done = false;
-    if (!attr_done && smem) {
+    if (smem)  // per device and cheap: set on every launch (one process may drive several GPUs)
         SHB_TRY_CUDA(cudaFuncSetAttribute(dft_kernel<R, UNIF, TILED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
-        attr_done = true;
-    }
     const uint64_t per_blk = (uint64_t)DFT_THREADS * K;
     const uint64_t nblk = (a.c_count + per_blk - 1) / per_blk;
     if (nblk > 0x7FFFFFFFull) return set_error(SHB_EINVAL, "too many outputs for one launch");
@@ -612,12 +609,9 @@ template <bool UNIF>
 static int launch_dft_mma(MmaArgs a, cudaStream_t st)
 {
     const size_t smem = UNIF ? 0 : (size_t)DFT_STAGES * MMA_CHUNK * sizeof(double2);
-    static bool attr_done = false;
-    if (!attr_done && smem) {
+    if (smem)
         SHB_TRY_CUDA(cudaFuncSetAttribute(dft_mma_kernel<UNIF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
-        attr_done = true;
-    }
     const uint64_t nblk = (a.c_count + MMA_OUT_PER_CTA - 1) / MMA_OUT_PER_CTA;
     if (nblk > 0x7FFFFFFFull) return set_error(SHB_EINVAL, "too many outputs for one launch");
     const unsigned nthreads = UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32;

@@ -185,12 +185,8 @@ extern "C" int shb_class_counts(const uint32_t *d_residues, uint64_t count, uint
     SHB_TRY_CUDA(cudaMemsetAsync(bad.ptr, 0, sizeof(unsigned int), st));
     const size_t smem = ncls * sizeof(uint32_t);
     if (smem <= 200 * 1024) {
-        static bool attr_set = false;
-        if (!attr_set) {
-            SHB_TRY_CUDA(cudaFuncSetAttribute(class_counts_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              200 * 1024));
-            attr_set = true;
-        }
+        SHB_TRY_CUDA(cudaFuncSetAttribute(class_counts_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          200 * 1024));
         const uint64_t per_block = (uint64_t)HIST_THREADS * 4 * 16;
         uint64_t blocks = (count + per_block - 1) / per_block;
         const uint64_t cap = (uint64_t)sm_count();

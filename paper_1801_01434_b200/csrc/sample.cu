@@ -500,12 +500,8 @@ static size_t seq_smem() { return sizeof(SeqShared); }
 
 static int seq_prepare()
 {
-    static bool done = false;
-    if (!done) {
-        SHB_TRY_CUDA(cudaFuncSetAttribute(seqscan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)seq_smem()));
-        done = true;
-    }
+    SHB_TRY_CUDA(cudaFuncSetAttribute(seqscan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)seq_smem()));
     return SHB_OK;
 }
 
