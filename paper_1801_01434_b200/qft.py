@@ -149,6 +149,13 @@ def _run(state, q: int, tiles: int, precision: str):
     return spec.numpy() if host else spec
 
 
+def _check_length(state, q: int) -> None:
+    """The reference validates the state length before the plan (qft.py:273-276)."""
+    n = (state.q,) if isinstance(state, dev.DeviceVector) else np.shape(state)
+    if tuple(n) != (q,):
+        raise ValueError(f"state length {tuple(n)} does not match q={q}")
+
+
 def dense_dft(state, tw: TwiddleTable, plan: KernelPlan):
     """Direct DFT, untiled (qft.py:270-287), on the GPU.
 
@@ -156,6 +163,7 @@ def dense_dft(state, tw: TwiddleTable, plan: KernelPlan):
     part returns a DeviceSpectrum that stays on the GPU.
     """
     q = tw.q
+    _check_length(state, q)
     plan = plan.resolved(q)
     if plan.tiles != 1:
         raise ValueError("dense_dft is untiled; use tiled_dft for tiles >= 2")
@@ -165,6 +173,7 @@ def dense_dft(state, tw: TwiddleTable, plan: KernelPlan):
 def tiled_dft(state, tw: TwiddleTable, plan: KernelPlan):
     """Split-K DFT (qft.py:290-317): input segments reduced in ascending order."""
     q = tw.q
+    _check_length(state, q)
     plan = plan.resolved(q)
     if plan.tiles < 2:
         raise ValueError("tiled_dft needs tiles >= 2; use dense_dft otherwise")

@@ -83,6 +83,11 @@ def test_qft_validation():
         qft.tiled_dft(np.zeros(16, complex), qft.build_twiddles(16), qft.KernelPlan())
     with pytest.raises(ValueError, match="capped"):
         qft.circuit_qft(np.zeros(1 << 13, complex))
+    # length is checked before the plan, as in the reference (qft.py:273-276)
+    with pytest.raises(ValueError, match="does not match q=16"):
+        qft.dense_dft(np.zeros(8, complex), qft.build_twiddles(16), qft.KernelPlan(block_size=3))
+    with pytest.raises(ValueError, match="does not match q=16"):
+        qft.tiled_dft(np.zeros(8, complex), qft.build_twiddles(16), qft.KernelPlan(tiles=3))
 
 
 def test_shor_driver_host_parts():
