@@ -69,8 +69,11 @@ struct Prec<double> {
     static constexpr uint64_t SEG = 8192;  // terms between exact re-seeds
 };
 template <>
+#ifndef SHB_DFT_K32
+#define SHB_DFT_K32 4
+#endif
 struct Prec<float> {
-    static constexpr int K = 4;
+    static constexpr int K = SHB_DFT_K32;
     static constexpr uint64_t SEG = 256;
 };
 
