@@ -301,14 +301,39 @@ static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t i
         int uni = 0;
         double ur = 0.0, ui = 0.0;
         if (len) SHB_TRY(shb_progression_is_uniform((const double *)d_amps.ptr, len, &uni, &ur, &ui, st));
-        if (uni)
-            rc = shb_dft_uniform(ur, ui, len, a0 + index_base, stride, q, c_begin, c_count, tiles, scale,
-                                 precision, (double *)d_out.ptr, nullptr, nullptr, st);
-        else
-            rc = shb_dft((const double *)d_amps.ptr, len, a0 + index_base, stride, q, c_begin, c_count,
-                         tiles, scale, precision, (double *)d_out.ptr, nullptr, nullptr, st);
+        // output slices: slice i's D2H copy (second stream) overlaps slice i+1's
+        // DFT.  Outputs are independent sums, so slicing changes no value.
+        const int nslice = c_count >= (1ull << 22) ? 8 : 1;
+        cudaStream_t cp = nullptr;
+        SHB_TRY_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+        StreamGuard cp_guard{cp};
+        cudaEvent_t ev[8];
+        for (int i = 0; i < nslice; i++) SHB_TRY_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        struct EventGuard {
+            cudaEvent_t *e;
+            int n;
+            ~EventGuard() {
+                for (int i = 0; i < n; i++) cudaEventDestroy(e[i]);
+            }
+        } ev_guard{ev, nslice};
+        double *dout = (double *)d_out.ptr;
+        for (int i = 0; i < nslice && rc == SHB_OK; i++) {
+            const uint64_t lo = c_count * i / nslice, hi = c_count * (i + 1) / nslice;
+            if (uni)
+                rc = shb_dft_uniform(ur, ui, len, a0 + index_base, stride, q, c_begin + lo, hi - lo, tiles,
+                                     scale, precision, dout + 2 * lo, nullptr, nullptr, st);
+            else
+                rc = shb_dft((const double *)d_amps.ptr, len, a0 + index_base, stride, q, c_begin + lo, hi - lo,
+                             tiles, scale, precision, dout + 2 * lo, nullptr, nullptr, st);
+            if (rc != SHB_OK) break;
+            SHB_TRY_CUDA(cudaEventRecord(ev[i], st));
+            SHB_TRY_CUDA(cudaStreamWaitEvent(cp, ev[i], 0));
+            SHB_TRY_CUDA(cudaMemcpyAsync(out_host + 2 * lo, dout + 2 * lo, (hi - lo) * 16, cudaMemcpyDeviceToHost,
+                                         cp));
+        }
+        SHB_TRY_CUDA(cudaStreamSynchronize(cp));
+        SHB_TRY_CUDA(cudaStreamSynchronize(st));
         if (rc != SHB_OK) return rc;
-        SHB_TRY_CUDA(cudaMemcpyAsync(out_host, d_out.ptr, c_count * 16, cudaMemcpyDeviceToHost, st));
     }
     SHB_TRY_CUDA(cudaStreamSynchronize(st));
     return rc;
