@@ -46,7 +46,7 @@ uint64_t shb_kernel_launches(void);
 int shb_fp64_peak(double seconds, double *tflops, void *stream);
 
 /* ------------------------------------------------------------------ modexp
- * qstate.entangle_modexp (qstate.py:94-113): part 2 of the register.
+ * qstate.entangle_modexp (qstate.py:64-83): part 2 of the register.
  * d_residues[i] = x^(a_begin + i) mod n for i < count, n in [2, 2^32).
  * Sharding: rank g passes its own a_begin / count slice.
  */
@@ -54,7 +54,7 @@ int shb_modexp(uint32_t *d_residues, uint64_t a_begin, uint64_t count,
                uint64_t x, uint64_t n, void *stream);
 
 /* ---------------------------------------------------------------- collapse
- * qstate.measure_part2 (qstate.py:125-127): np.bincount of residue classes
+ * qstate.measure_part2 (qstate.py:95-97): np.bincount of residue classes
  * with the (uniform) weights factored out -> exact integer class counts.
  * d_counts[v] += #{i : d_residues[i] == v}; accumulates, so shards can add
  * into one buffer.  d_counts must hold ncls entries (ncls > max residue).
@@ -62,7 +62,7 @@ int shb_modexp(uint32_t *d_residues, uint64_t a_begin, uint64_t count,
 int shb_class_counts(const uint32_t *d_residues, uint64_t count,
                      uint64_t *d_counts, uint64_t ncls, void *stream);
 
-/* qstate.measure_part2 (qstate.py:131): mask = residues == k.
+/* qstate.measure_part2 (qstate.py:101): mask = residues == k.
  * Writes the ascending indices a_begin + i with d_residues[i] == k into
  * d_support (capacity entries) by warp-ballot + prefix-sum compaction and
  * returns their number in *m_out (host).  SHB_ERANGE if capacity < M.
@@ -107,9 +107,9 @@ int shb_fill_progression(const uint64_t *d_support, uint64_t m, uint64_t a0,
  *   a_j = a0 + j*stride (j < length),  c = c_begin + i (i < c_count)
  *
  * tile t covers a in [t*q/tiles, (t+1)*q/tiles); tile partials are added in
- * ascending t (qft.py:313-315).  Only the support is visited: q*M phase terms.
+ * ascending t (qft.py:138-141).  Only the support is visited: q*M phase terms.
  * d_amps: complex128[length]; d_out: complex128[c_count];
- * d_prob (nullable): float64[c_count] = |out|^2 as np.abs(.)**2 (qstate.py:141);
+ * d_prob (nullable): float64[c_count] = |out|^2 as np.abs(.)**2 (qstate.py:111);
  * d_block_sums (nullable): per-CTA sums of d_prob, see shb_dft_num_blocks.
  * precision: SHB_FP64 (<=1e-9 relative) or SHB_FP32 (<=1e-4 relative).
  * Sharding: rank g passes its own c_begin / c_count.
@@ -122,7 +122,7 @@ uint64_t shb_dft_num_blocks(uint64_t c_count, int precision);
 
 /* Same transform for a uniform comb: every one of the `length` progression
  * amplitudes equals (amp_re + i amp_im) -- the collapsed register of
- * measure_part2 (qstate.py:131-134).  The amplitude is factored
+ * measure_part2 (qstate.py:101-104).  The amplitude is factored
  * out of the sum (out = scale * amp * sum_j e^{...}); no amplitude array. */
 int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, uint64_t a0,
                     uint64_t stride, uint64_t q, uint64_t c_begin,
@@ -131,9 +131,9 @@ int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, uint64_t a0,
                     double *d_block_sums, void *stream);
 
 /* ---------------------------------------------------------------- sampling
- * qstate.sample_part1 / l2_norm (qstate.py:138-148).
+ * qstate.sample_part1 / l2_norm (qstate.py:108-118).
  */
-/* d_prob[i] = |d_state[i]|^2 computed as hypot(re, im)^2 (qstate.py:141). */
+/* d_prob[i] = |d_state[i]|^2 computed as hypot(re, im)^2 (qstate.py:111). */
 int shb_probabilities(const double *d_state, uint64_t count, double *d_prob,
                       void *stream);
 
@@ -141,16 +141,16 @@ int shb_probabilities(const double *d_state, uint64_t count, double *d_prob,
 int shb_sum(const double *d_x, uint64_t count, double *out, void *stream);
 
 /* Exact emulation of np.cumsum(p)[-1] (strict left-to-right float64 adds,
- * qstate.py:142): bit-identical to numpy for any input. */
+ * qstate.py:112): bit-identical to numpy for any input. */
 int shb_cumsum_total(const double *d_prob, uint64_t count, double *total,
                      void *stream);
 
 /* Exact emulation of np.searchsorted(np.cumsum(p), target, side="right")
- * (qstate.py:143): first i with cumsum[i] > target, or count if none. */
+ * (qstate.py:113): first i with cumsum[i] > target, or count if none. */
 int shb_cumsum_search(const double *d_prob, uint64_t count, double target,
                       uint64_t *index, void *stream);
 
-/* The whole Born-rule read (qstate.py:142-144) for a draw u:
+/* The whole Born-rule read (qstate.py:112-114) for a draw u:
  * target = u * cumsum[-1], *index = searchsorted(cumsum, target, "right")
  * (un-clamped; the caller clamps to q-1), *total = cumsum[-1] (nullable). */
 int shb_sample_index(const double *d_prob, uint64_t count, double u,
@@ -178,9 +178,9 @@ int shb_partial_row_sums_host(double *out, const double *state,
  * measure_part2 for odd register widths where 1/sqrt(q) is inexact.
  */
 /* np.cumsum(np.full(count, w))[-1] == the per-bin accumulation of
- * np.bincount(weights=...) (qstate.py:127) for uniform weights. */
+ * np.bincount(weights=...) (qstate.py:97) for uniform weights. */
 double shb_host_seqsum_const(double w, uint64_t count);
-/* np.full(count, w).sum() (numpy pairwise summation, qstate.py:132). */
+/* np.full(count, w).sum() (numpy pairwise summation, qstate.py:102). */
 double shb_host_pairwise_sum_const(double w, uint64_t count);
 
 #ifdef __cplusplus

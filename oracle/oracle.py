@@ -67,7 +67,7 @@ def default_threads() -> int:
 # ---------------------------------------------------------------- twiddles
 
 def roots(q: int, idx) -> np.ndarray:
-    """Entries of qft.build_twiddles(q).roots at `idx` (qft.py:254), bitwise."""
+    """Entries of qft.build_twiddles(q).roots at `idx` (qft.py:79), bitwise."""
     idx = np.ascontiguousarray(idx, dtype=np.uint64)
     out = np.empty(2 * idx.size, dtype=np.float64)
     lib().oracle_roots(q, idx.size, _ptr(idx), _ptr(out))
@@ -78,11 +78,11 @@ def roots(q: int, idx) -> np.ndarray:
 
 def dft_rows(state_support, amps, q: int, rows, scale: bool = True,
              threads: int | None = None) -> np.ndarray:
-    """Rows `rows` of qft.dense_dft (qft.py:270-287 / _kernels.py:16-30).
+    """Rows `rows` of qft.dense_dft (qft.py:95-112 / _kernels.py:16-30).
 
     `state_support` are the ascending indices of the nonzero amplitudes and
     `amps` their complex values.  With scale=True the 1/sqrt(q) factor is
-    applied exactly as qft.py:286 does; bitwise identical to the reference.
+    applied exactly as qft.py:111 does; bitwise identical to the reference.
     """
     supp = np.ascontiguousarray(state_support, dtype=np.uint64)
     a = np.ascontiguousarray(amps, dtype=np.complex128)
@@ -108,7 +108,7 @@ def dense_dft(state: np.ndarray, threads: int | None = None) -> np.ndarray:
 
 
 def tiled_dft(state: np.ndarray, tiles: int, threads: int | None = None) -> np.ndarray:
-    """Reference tiled_dft (qft.py:290-317): per-segment partials, ascending add."""
+    """Reference tiled_dft (qft.py:115-142): per-segment partials, ascending add."""
     state = np.ascontiguousarray(state, dtype=np.complex128)
     q = state.size
     seg = q // tiles
@@ -138,14 +138,14 @@ def dense_rows_literal(state: np.ndarray, rows, j0: int = 0, j1: int | None = No
 # ---------------------------------------------------------------- modexp
 
 def modexp_residues(x: int, n: int, q: int, a_begin: int = 0) -> np.ndarray:
-    """entangle_modexp residues (qstate.py:94-113) as uint32, by recurrence."""
+    """entangle_modexp residues (qstate.py:64-83) as uint32, by recurrence."""
     out = np.empty(q, dtype=np.uint32)
     lib().oracle_modexp(x, n, a_begin, q, _ptr(out))
     return out
 
 
 def modexp_residues_cycle(x: int, n: int, q: int) -> np.ndarray:
-    """The reference's own construction: one cycle of x^a, tiled to q (qstate.py:107-112)."""
+    """The reference's own construction: one cycle of x^a, tiled to q (qstate.py:77-82)."""
     seq = [1 % n]
     v = x % n
     while v != 1 % n:
@@ -164,7 +164,7 @@ def class_counts(residues: np.ndarray, ncls: int) -> np.ndarray:
 
 
 def measure_part2(amplitudes: np.ndarray, residues: np.ndarray, u: float):
-    """qstate.measure_part2 (qstate.py:116-135) on host arrays with draw u.
+    """qstate.measure_part2 (qstate.py:86-105) on host arrays with draw u.
 
     Returns (k, collapsed amplitude vector).
     """
@@ -185,12 +185,12 @@ def measure_part2(amplitudes: np.ndarray, residues: np.ndarray, u: float):
 # ---------------------------------------------------------------- sampling
 
 def probabilities(spectrum: np.ndarray) -> np.ndarray:
-    """|amp|**2 as qstate.py:141 computes it (np.abs -> hypot, then square)."""
+    """|amp|**2 as qstate.py:111 computes it (np.abs -> hypot, then square)."""
     return np.abs(np.asarray(spectrum, dtype=np.complex128)) ** 2
 
 
 def sample_index(probs: np.ndarray, u: float) -> int:
-    """qstate.sample_part1 tail (qstate.py:142-144) via the C sequential scan."""
+    """qstate.sample_part1 tail (qstate.py:112-114) via the C sequential scan."""
     p = np.ascontiguousarray(probs, dtype=np.float64)
     return int(lib().oracle_cumsum_search(_ptr(p), p.size, u, None))
 

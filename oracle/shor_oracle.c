@@ -60,7 +60,7 @@ static void oracle_parallel_for(int64_t n, int nthreads,
 
 /*
  * roots[idx] exactly as qft.build_twiddles builds its table
- * (qft.py:254: np.exp((2j*np.pi/q) * np.arange(q))).
+ * (qft.py:79: np.exp((2j*np.pi/q) * np.arange(q))).
  * (2j*pi/q) is the complex (0, fl(2*pi)/q); multiplying by (idx + 0j) gives
  * (0, fl(t*idx)); numpy's exp of a purely imaginary argument is
  * (cos(y), sin(y)) from libm.  Checked bitwise against numpy on every width
@@ -84,9 +84,9 @@ void oracle_roots(uint64_t q, uint64_t n, const uint64_t *idx, double *out)
  * Rows of the reference dense transform restricted to the support.
  *
  * Reference: _kernels.partial_row_sums (_kernels.py:16-30) called by
- * qft.dense_dft (qft.py:270-287) with j0=0, j1=q:
+ * qft.dense_dft (qft.py:95-112) with j0=0, j1=q:
  *     acc = 0; for j ascending: acc += roots[(j*k) mod q] * state[j]
- * then out *= 1/sqrt(q) (qft.py:286).
+ * then out *= 1/sqrt(q) (qft.py:111).
  * Terms with state[j] == 0 add an exact (+-0, +-0) and leave acc unchanged,
  * so summing over the nonzero support only, in ascending order, is bitwise
  * identical to the reference (pinned by the n=15 / n=221 golden spectra).
@@ -192,7 +192,7 @@ void oracle_dense_rows_literal(uint64_t q, const double *state, uint64_t j0,
 /*
  * residues[i] = x^(a_begin + i) mod n, by the incremental recurrence the
  * SPEC states for entangle_modexp (the reference walks one
- * cycle and tiles it, qstate.py:107-112, which yields the same values).
+ * cycle and tiles it, qstate.py:77-82, which yields the same values).
  */
 void oracle_modexp(uint64_t x, uint64_t n, uint64_t a_begin, uint64_t count,
                    uint32_t *residues)
@@ -213,7 +213,7 @@ void oracle_modexp(uint64_t x, uint64_t n, uint64_t a_begin, uint64_t count,
     }
 }
 
-/* bincount of residues (qstate.py:127) with unit weights: exact counts */
+/* bincount of residues (qstate.py:97) with unit weights: exact counts */
 void oracle_class_counts(const uint32_t *residues, uint64_t count,
                          uint64_t ncls, uint64_t *counts)
 {
@@ -222,7 +222,7 @@ void oracle_class_counts(const uint32_t *residues, uint64_t count,
 }
 
 /*
- * qstate.sample_part1 tail (qstate.py:142-144):
+ * qstate.sample_part1 tail (qstate.py:112-114):
  *   cum = np.cumsum(probs)            -- strictly sequential float64 adds
  *   m = searchsorted(cum, u*cum[-1], side="right"); min(m, q-1)
  */

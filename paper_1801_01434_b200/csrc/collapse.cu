@@ -1,5 +1,5 @@
 // Stage 2 of the hot path: measurement collapse of part 2
-// (qstate.measure_part2, qstate.py:116-135) -- stream compaction of
+// (qstate.measure_part2, qstate.py:86-105) -- stream compaction of
 // {a : residues[a] == k} -- and the support-geometry reductions that turn a
 // support (or the nonzero pattern of a dense state) into the arithmetic
 // progression the DFT kernel walks.

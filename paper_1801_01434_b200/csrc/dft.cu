@@ -16,7 +16,7 @@
 //   segment value = e^{2 pi i a_last c / q} * acc   (exact sincospi re-seed)
 //
 // Segments are re-seeded every SEG terms (rounding growth <= SEG*eps) and
-// tile partials (reference tiles, qft.py:306-316) are added in ascending
+// tile partials (reference tiles, qft.py:131-141) are added in ascending
 // tile order.  Each thread owns K outputs (K independent FMA chains).
 //
 // Two instantiations, selected from the data by the caller:
@@ -31,7 +31,7 @@
 //    bank), which keeps every FP64 instruction at <= 2 register-file operand
 //    reads -- the generic step needs 3 and is register-bandwidth bound.
 //
-// The epilogue fuses |V|^2 (hypot^2, as np.abs(.)**2, qstate.py:141) and a
+// The epilogue fuses |V|^2 (hypot^2, as np.abs(.)**2, qstate.py:111) and a
 // deterministic per-CTA sum of it (norm check, qstate.py:50-53).
 #include <math.h>
 #include <stdlib.h>
@@ -363,7 +363,7 @@ static int launch_dft_t(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t
 template <typename R, bool UNIF>
 static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t st)
 {
-    // tile partials only exist for the reference's tiled engine (qft.py:290-317)
+    // tile partials only exist for the reference's tiled engine (qft.py:115-142)
     return tiles > 1 ? launch_dft_t<R, UNIF, true>(a, length, tiles, st)
                      : launch_dft_t<R, UNIF, false>(a, length, tiles, st);
 }

@@ -1,6 +1,6 @@
 // Stage 1 of the hot path: part 2 of the register, residues[a] = x^a mod n
-// (qstate.entangle_modexp, qstate.py:94-113), plus the exact residue-class
-// histogram that measure_part2 needs (qstate.py:125-127).
+// (qstate.entangle_modexp, qstate.py:64-83), plus the exact residue-class
+// histogram that measure_part2 needs (qstate.py:95-97).
 //
 // HBM-bound: 4 bytes written per exponent (uint32 residues; n < 2^32).
 // Each warp owns a contiguous span of exponents; lane l seeds x^(a0+l) by

@@ -1,5 +1,5 @@
 // Stage 4 (tail of the hot path): Born-rule read of part 1
-// (qstate.sample_part1 / l2_norm, qstate.py:138-148).
+// (qstate.sample_part1 / l2_norm, qstate.py:108-118).
 //
 //   probs = np.abs(amp)**2 ; cum = np.cumsum(probs)
 //   m = searchsorted(cum, u*cum[-1], side="right")
@@ -635,6 +635,6 @@ extern "C" int shb_sample_index(const double *d_prob, uint64_t count, double u, 
     double tot = 0.0;
     SHB_TRY(seq_total(d_prob, count, (double *)cs.ptr, &tot, st));
     if (total) *total = tot;
-    const double target = u * tot;  // s.uniform() * cum[-1] (qstate.py:143)
+    const double target = u * tot;  // s.uniform() * cum[-1] (qstate.py:113)
     return search_from_tiles(d_prob, count, (const double *)cs.ptr, tot, target, index, st);
 }

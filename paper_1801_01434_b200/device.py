@@ -1,6 +1,6 @@
 """Device-resident register parts and thin wrappers over the C ABI.
 
-The reference keeps the register as two numpy arrays (qstate.py:65-72).  At
+The reference keeps the register as two numpy arrays (qstate.py:36-42).  At
 q = 2^30 those are 16 GiB + 8 GiB and every stage would round-trip them
 through host memory, so the B200 path keeps them on the GPU and exposes
 them through ``DeviceVector``: an array-like whose ``__array__`` copies to
@@ -263,7 +263,7 @@ class DeviceVector:
 
 
 class UniformAmplitudes(DeviceVector):
-    """1/sqrt(q) everywhere (qstate.init_uniform, qstate.py:86-91); never stored."""
+    """1/sqrt(q) everywhere (qstate.init_uniform, qstate.py:56-61); never stored."""
 
     def __init__(self, q: int):
         super().__init__(q)
@@ -281,7 +281,7 @@ class ZeroResidues(DeviceVector):
 
 
 class DeviceResidues(DeviceVector):
-    """x^a mod n as uint32 on the device (int64 on the host, qstate.py:69)."""
+    """x^a mod n as uint32 on the device (int64 on the host, qstate.py:39)."""
 
     dtype = np.dtype(np.int64)
 

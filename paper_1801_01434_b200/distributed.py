@@ -206,7 +206,7 @@ def sharded_attempt(n: int, x: int, q: int, sampler: qstate.Sampler, *, rank: in
 
 def dump_spectrum_sharded(out, q: int, path, *, rank: int = 0, world: int = 1, group=None,
                           chunk_elems: int = 1 << 22) -> None:
-    """QREG dump (qstate.dump_state format, qstate.py:151-160) of a c-sharded
+    """QREG dump (qstate.dump_state format, qstate.py:121-130) of a c-sharded
     spectrum: rank 0 writes the 16-byte header and sizes the file, then every
     rank writes its own slice [g q/G, (g+1) q/G) at its byte offset in 64 MiB
     pieces.  `out` is this rank's float64 [2 * shard] (interleaved re, im)

@@ -150,14 +150,14 @@ def _run(state, q: int, tiles: int, precision: str):
 
 
 def _check_length(state, q: int) -> None:
-    """The reference validates the state length before the plan (qft.py:273-276)."""
+    """The reference validates the state length before the plan (qft.py:98-101)."""
     n = (state.q,) if isinstance(state, dev.DeviceVector) else np.shape(state)
     if tuple(n) != (q,):
         raise ValueError(f"state length {tuple(n)} does not match q={q}")
 
 
 def dense_dft(state, tw: TwiddleTable, plan: KernelPlan):
-    """Direct DFT, untiled (qft.py:270-287), on the GPU.
+    """Direct DFT, untiled (qft.py:95-112), on the GPU.
 
     A numpy input returns a numpy array (drop-in); a device-resident register
     part returns a DeviceSpectrum that stays on the GPU.
@@ -171,7 +171,7 @@ def dense_dft(state, tw: TwiddleTable, plan: KernelPlan):
 
 
 def tiled_dft(state, tw: TwiddleTable, plan: KernelPlan):
-    """Split-K DFT (qft.py:290-317): input segments reduced in ascending order."""
+    """Split-K DFT (qft.py:115-142): input segments reduced in ascending order."""
     q = tw.q
     _check_length(state, q)
     plan = plan.resolved(q)

@@ -74,13 +74,13 @@ def _require_normalized(reg: CompositeRegister) -> None:
 
 
 def init_uniform(q: int) -> CompositeRegister:
-    """(1/sqrt q) sum_a |a, 0> (qstate.py:86-91); the constant is never stored."""
+    """(1/sqrt q) sum_a |a, 0> (qstate.py:56-61); the constant is never stored."""
     _require_power_of_two(q)
     return CompositeRegister(q=q, amplitudes=dev.UniformAmplitudes(q), residues=dev.ZeroResidues(q))
 
 
 def entangle_modexp(reg: CompositeRegister, x: int, n: int) -> CompositeRegister:
-    """residues[a] = x**a mod n for every a (qstate.py:94-113), on the GPU."""
+    """residues[a] = x**a mod n for every a (qstate.py:64-83), on the GPU."""
     if n < 2:
         raise ValueError("modulus must be >= 2")
     if math.gcd(x, n) != 1:
@@ -117,7 +117,7 @@ def _uniform_value(amps, q: int):
 
 
 def _class_probabilities(counts: np.ndarray, w0: float) -> np.ndarray:
-    """np.bincount(res, weights=full(q, w0)) from exact counts (qstate.py:127).
+    """np.bincount(res, weights=full(q, w0)) from exact counts (qstate.py:97).
 
     bincount adds each bin's weights left to right, so bin v holds the
     sequential float64 sum of counts[v] copies of w0.
@@ -132,12 +132,12 @@ def _class_probabilities(counts: np.ndarray, w0: float) -> np.ndarray:
 
 
 def uniform_weight(a_unif: complex) -> float:
-    """|amp|^2 of the uniform amplitude, as np.abs(amp)**2 computes it (qstate.py:125)."""
+    """|amp|^2 of the uniform amplitude, as np.abs(amp)**2 computes it (qstate.py:95)."""
     return float(np.abs(np.array([a_unif], dtype=np.complex128))[0] ** 2)
 
 
 def draw_class(counts: np.ndarray, w0: float, u: float) -> int:
-    """Outcome k from exact class counts and the draw u (qstate.py:126-130)."""
+    """Outcome k from exact class counts and the draw u (qstate.py:96-100)."""
     nz = np.flatnonzero(counts)
     nclasses = int(nz[-1]) + 1
     probs = _class_probabilities(np.asarray(counts)[:nclasses], w0)
@@ -147,13 +147,13 @@ def draw_class(counts: np.ndarray, w0: float, u: float) -> int:
 
 
 def collapsed_amplitude(a_unif: complex, w0: float, M: int) -> complex:
-    """amp / sqrt(sum of the M kept weights) exactly as qstate.py:132-134 rounds it."""
+    """amp / sqrt(sum of the M kept weights) exactly as qstate.py:102-104 rounds it."""
     kept = np.sqrt(np.float64(nat.host_pairwise_sum_const(w0, M)))
     return complex((np.array([a_unif], dtype=np.complex128) / kept)[0])
 
 
 def measure_part2(reg: CompositeRegister, s: Sampler) -> tuple[int, CompositeRegister]:
-    """Observe part 2 and collapse part 1 onto {a : residue[a] == k} (qstate.py:116-135)."""
+    """Observe part 2 and collapse part 1 onto {a : residue[a] == k} (qstate.py:86-105)."""
     _require_normalized(reg)
     if reg.collapsed_k is not None:
         raise ValueError("part 2 was already measured")
@@ -175,7 +175,7 @@ def measure_part2(reg: CompositeRegister, s: Sampler) -> tuple[int, CompositeReg
 
 
 def _device_probabilities(reg: CompositeRegister):
-    """|amp|^2 of part 1 as a device float64 tensor (qstate.py:141)."""
+    """|amp|^2 of part 1 as a device float64 tensor (qstate.py:111)."""
     t = nat.require_cuda()
     a = reg.amplitudes
     if isinstance(a, dev.DeviceSpectrum):
@@ -193,15 +193,15 @@ def _device_probabilities(reg: CompositeRegister):
 
 
 def sample_part1(reg: CompositeRegister, s: Sampler) -> int:
-    """Born-rule read of part 1 (qstate.py:138-144), exact sequential CDF on the GPU."""
+    """Born-rule read of part 1 (qstate.py:108-114), exact sequential CDF on the GPU."""
     _require_normalized(reg)
     p = _device_probabilities(reg)
-    m, _ = dev.sample_index(p, s.uniform())  # target = u * cum[-1], as qstate.py:143
+    m, _ = dev.sample_index(p, s.uniform())  # target = u * cum[-1], as qstate.py:113
     return min(m, reg.q - 1)
 
 
 def l2_norm(reg: CompositeRegister) -> float:
-    """sqrt(sum |amp|^2) (qstate.py:147-148)."""
+    """sqrt(sum |amp|^2) (qstate.py:117-118)."""
     a = reg.amplitudes
     if isinstance(a, dev.UniformAmplitudes):
         return math.sqrt(a.q) * abs(a.value)
@@ -213,7 +213,7 @@ def l2_norm(reg: CompositeRegister) -> float:
 
 
 def dump_state(reg: CompositeRegister, path) -> None:
-    """QREG dump: 16-byte header + q little-endian complex128 (qstate.py:151-160).
+    """QREG dump: 16-byte header + q little-endian complex128 (qstate.py:121-130).
 
     Device spectra are streamed to the file in 64 MiB slices, never as one
     host copy of the whole register.
@@ -233,7 +233,7 @@ def dump_state(reg: CompositeRegister, path) -> None:
 
 
 def load_state(path) -> np.ndarray:
-    """Read a dump_state file back (qstate.py:163-175)."""
+    """Read a dump_state file back (qstate.py:133-145)."""
     with open(path, "rb") as fh:
         magic, version, w, _ = _DUMP_HEADER.unpack(fh.read(_DUMP_HEADER.size))
         if magic != _DUMP_MAGIC:

@@ -43,7 +43,7 @@ def test_entangle_validation_before_device_work():
 
 
 def test_measure_validation_order():
-    # unnormalized first (qstate.py:122), then already-measured (qstate.py:123)
+    # unnormalized first (qstate.py:92), then already-measured (qstate.py:93)
     reg = qstate.CompositeRegister(q=4, amplitudes=np.full(4, 0.7, complex), residues=np.zeros(4, np.int64))
     with pytest.raises(ValueError, match="not normalized"):
         qstate.measure_part2(reg, qstate.Sampler(0))
@@ -83,7 +83,7 @@ def test_qft_validation():
         qft.tiled_dft(np.zeros(16, complex), qft.build_twiddles(16), qft.KernelPlan())
     with pytest.raises(ValueError, match="capped"):
         qft.circuit_qft(np.zeros(1 << 13, complex))
-    # length is checked before the plan, as in the reference (qft.py:273-276)
+    # length is checked before the plan, as in the reference (qft.py:98-101)
     with pytest.raises(ValueError, match="does not match q=16"):
         qft.dense_dft(np.zeros(8, complex), qft.build_twiddles(16), qft.KernelPlan(block_size=3))
     with pytest.raises(ValueError, match="does not match q=16"):

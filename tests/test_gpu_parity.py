@@ -150,7 +150,7 @@ def test_dft_vs_reference_rows(golden_dir, tag):
     if q <= (1 << 16):
         out, prob, _ = dev.dft(amps, M, c0, r, q, 0, q)
         _check_spectrum(_rows(out, rows), d["V"])
-        # fused probabilities are hypot(re, im)^2 (qstate.py:141); CUDA's hypot
+        # fused probabilities are hypot(re, im)^2 (qstate.py:111); CUDA's hypot
         # is not glibc's, so equal to within a few ulp rather than bitwise
         p_host = prob.cpu().numpy()
         p_np = np.abs(out.cpu().numpy().view(np.complex128)) ** 2

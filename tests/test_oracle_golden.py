@@ -29,7 +29,7 @@ def test_root_table_bitwise(kats):
         got = oracle.roots(q, np.arange(q))
         ref = np.array([complex(a, b) for a, b in vals])
         assert np.array_equal(got.view(np.float64), ref.view(np.float64))
-    # wide tables: compare with numpy's own expression (qft.py:254) on samples
+    # wide tables: compare with numpy's own expression (qft.py:79) on samples
     for w in (16, 24, 30, 32):
         q = 1 << w
         idx = np.random.default_rng(w).integers(0, q, 20000, dtype=np.uint64)
