@@ -28,7 +28,8 @@ enum shb_status {
     SHB_EINVAL = 1, /* argument error      -> ValueError in the Python layer */
     SHB_ECUDA = 2,  /* CUDA runtime error  -> RuntimeError                   */
     SHB_ENOMEM = 3, /* device allocation   -> MemoryError                    */
-    SHB_ERANGE = 4  /* capacity too small  -> ValueError                     */
+    SHB_ERANGE = 4, /* capacity too small  -> ValueError                     */
+    SHB_EIO = 5     /* file I/O            -> OSError                        */
 };
 
 enum shb_precision { SHB_FP64 = 0, SHB_FP32 = 1 };
@@ -100,7 +101,7 @@ int shb_fill_progression(const uint64_t *d_support, uint64_t m, uint64_t a0,
                          double amp_im, double *d_amps, void *stream);
 
 /* --------------------------------------------------------------------- QFT
- * qft.dense_dft / qft.tiled_dft (qft.py:270-317) and the compiled inner loop
+ * qft.dense_dft / qft.tiled_dft (qft.py:95-142) and the compiled inner loop
  * _kernels.partial_row_sums (_kernels.py:16-30), B200 form:
  *
  *   out[i] = scale * sum_{t < tiles} sum_{a_j in tile t} amps[j] e^{+2 pi i a_j c / q}
@@ -173,10 +174,95 @@ int shb_partial_row_sums_host(double *out, const double *state,
                               const double *roots, uint64_t q, uint64_t k0,
                               uint64_t k1, uint64_t j0, uint64_t j1);
 
+/* ------------------------------------------------- register handle (ctx)
+ * The whole attempt of shor.single_attempt (shor.py:73-133) on one opaque
+ * register that owns its device memory, for FFI callers that hold no device
+ * pointers.  The register is sharded over the handle's
+ * devices: part 2 (residues) by index a, the spectrum by output c.  One host
+ * thread drives every shard; the only cross-shard exchanges are the class
+ * counts (host sum), the support geometry (host gcd) and, for sampling, a
+ * peer copy of the probabilities to the first shard's device.
+ *
+ * Stage order (each call checks it, SHB_EINVAL otherwise):
+ *   shb_init -> shb_ctx_modexp          init_uniform + entangle_modexp (qstate.py:56-83)
+ *            -> shb_measure(u) | shb_ctx_class_counts + shb_collapse(k)
+ *                                        measure_part2 (qstate.py:86-105)
+ *            -> shb_ctx_dft              qft.transform "dense"/"tiled" (qft.py:95-142)
+ *            -> shb_sample(u)            sample_part1 (qstate.py:108-114)
+ * shb_norm, the shb_copy_* readers and shb_dump_state work at any stage that
+ * has the data.  A handle is not reentrant: one handle per concurrent run.
+ */
+typedef struct shb_ctx shb_ctx;
+
+/* Handle over devices 0..ngpu-1 (ngpu <= 0: every visible device). */
+int shb_init(int ngpu, shb_ctx **ctx);
+/* Handle over an explicit device list; a device may repeat (several shards
+ * on one device, e.g. to exercise the sharded path on a single GPU). */
+int shb_init_devices(const int *devices, int ndev, shb_ctx **ctx);
+void shb_free(shb_ctx *ctx);
+/* *stage: 0 empty, 1 entangled, 2 collapsed, 3 transformed; *q register
+ * size, *n modulus (0 before shb_ctx_modexp).  Outputs are nullable. */
+int shb_ctx_state(const shb_ctx *ctx, int *stage, uint64_t *q, uint64_t *n,
+                  int *nshards);
+
+/* init_uniform(2^w) then entangle_modexp(reg, x, n) (qstate.py:56-83):
+ * residues[a] = x^a mod n on the shards.  Same ValueErrors as the reference
+ * (n < 2, gcd(x, n) != 1); w in [1, 32].  Discards any previous register. */
+int shb_ctx_modexp(shb_ctx *ctx, uint64_t x, uint64_t n, uint32_t w);
+
+/* Exact residue-class counts of part 2 (the integer form of the bincount at
+ * qstate.py:97): counts_out[v] for v < ncls; ncls must be >= n (SHB_ERANGE). */
+int shb_ctx_class_counts(shb_ctx *ctx, uint64_t *counts_out, uint64_t ncls);
+
+/* Collapse part 1 onto {a : residue[a] == k} (qstate.py:101-104): *M_out =
+ * support size, *amp_out = the surviving amplitude (real; imaginary part +0),
+ * rounded exactly as the reference divides by sqrt(sum of kept weights). */
+int shb_collapse(shb_ctx *ctx, uint32_t k, uint64_t *M_out, double *amp_out);
+
+/* measure_part2 with the draw u = s.uniform() (qstate.py:86-105): the
+ * outcome k from the exact class counts (shb_host_measure_class), then
+ * shb_collapse(k).  k, M and the amplitude are bit-identical to the
+ * reference. */
+int shb_measure(shb_ctx *ctx, double u, uint32_t *k_out, uint64_t *M_out,
+                double *amp_out);
+
+/* The QFT of the collapsed register (qft.dense_dft for tiles == 1,
+ * qft.tiled_dft for tiles >= 2, tiles | q), with |V|^2 fused. */
+int shb_ctx_dft(shb_ctx *ctx, int precision, uint32_t tiles);
+
+/* l2_norm (qstate.py:117-118) of the register at its current stage. */
+int shb_norm(shb_ctx *ctx, double *out);
+
+/* sample_part1 with the draw u (qstate.py:108-114) on the transformed
+ * register: norm check (1e-9 FP64, 1e-4 FP32), exact sequential cumsum,
+ * m = min(searchsorted(cum, u * cum[-1], "right"), q - 1). */
+int shb_sample(shb_ctx *ctx, double u, uint64_t *m_out);
+
+/* Host readers.  Spectrum rows [c0, c1) as interleaved complex128; the
+ * support (ascending, capacity entries; *m_out = M even on SHB_ERANGE);
+ * residues [a0, a1) widened to int64 like the reference array (qstate.py:39). */
+int shb_copy_spectrum(shb_ctx *ctx, uint64_t c0, uint64_t c1, double *host_out);
+int shb_copy_support(shb_ctx *ctx, uint64_t *host_out, uint64_t capacity,
+                     uint64_t *m_out);
+int shb_copy_residues(shb_ctx *ctx, uint64_t a0, uint64_t a1, int64_t *host_out);
+
+/* qstate.dump_state (qstate.py:121-130) of the transformed register:
+ * "QREG" header + q little-endian complex128, streamed shard by shard.
+ * SHB_EIO if the file cannot be written. */
+int shb_dump_state(shb_ctx *ctx, const char *path);
+
 /* --------------------------------------------- exact host-side helpers
  * Closed-form emulation of numpy reductions over a constant vector; used by
  * measure_part2 for odd register widths where 1/sqrt(q) is inexact.
  */
+/* The host half of measure_part2 (qstate.py:95-104) for the uniform register
+ * of size q, from exact class counts counts[0..ncls): nclasses = last
+ * nonzero class + 1; probs = bincount sums; k = min(searchsorted(cumsum,
+ * u * cum[-1], "right"), nclasses - 1); M = counts[k]; amplitude as numpy's
+ * complex division rounds it.  No device work. */
+int shb_host_measure_class(const uint64_t *counts, uint64_t ncls, uint64_t q,
+                           double u, uint32_t *k_out, uint64_t *M_out,
+                           double *amp_out);
 /* np.cumsum(np.full(count, w))[-1] == the per-bin accumulation of
  * np.bincount(weights=...) (qstate.py:97) for uniform weights. */
 double shb_host_seqsum_const(double w, uint64_t count);

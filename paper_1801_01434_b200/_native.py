@@ -16,7 +16,7 @@ import numpy as np
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libshorb200.so"
 
-SHB_OK, SHB_EINVAL, SHB_ECUDA, SHB_ENOMEM, SHB_ERANGE = 0, 1, 2, 3, 4
+SHB_OK, SHB_EINVAL, SHB_ECUDA, SHB_ENOMEM, SHB_ERANGE, SHB_EIO = 0, 1, 2, 3, 4, 5
 FP64, FP32 = 0, 1
 
 # every symbol include/shorb200.h declares, with its ctypes signature
@@ -49,6 +49,22 @@ SIGNATURES = {
     "shb_sample_index": ([_vp, _u64, _f64, _P64, _PF64, _vp], _i32),
     "shb_dense_dft_host": ([_vp, _u64, _u32, _i32, _vp], _i32),
     "shb_partial_row_sums_host": ([_vp, _vp, _vp, _u64, _u64, _u64, _u64, _u64], _i32),
+    "shb_init": ([_i32, ctypes.POINTER(_vp)], _i32),
+    "shb_init_devices": ([_vp, _i32, ctypes.POINTER(_vp)], _i32),
+    "shb_free": ([_vp], None),
+    "shb_ctx_state": ([_vp, ctypes.POINTER(ctypes.c_int), _P64, _P64, ctypes.POINTER(ctypes.c_int)], _i32),
+    "shb_ctx_modexp": ([_vp, _u64, _u64, _u32], _i32),
+    "shb_ctx_class_counts": ([_vp, _vp, _u64], _i32),
+    "shb_collapse": ([_vp, _u32, _P64, _PF64], _i32),
+    "shb_measure": ([_vp, _f64, ctypes.POINTER(ctypes.c_uint32), _P64, _PF64], _i32),
+    "shb_ctx_dft": ([_vp, _i32, _u32], _i32),
+    "shb_norm": ([_vp, _PF64], _i32),
+    "shb_sample": ([_vp, _f64, _P64], _i32),
+    "shb_copy_spectrum": ([_vp, _u64, _u64, _vp], _i32),
+    "shb_copy_support": ([_vp, _vp, _u64, _P64], _i32),
+    "shb_copy_residues": ([_vp, _u64, _u64, _vp], _i32),
+    "shb_dump_state": ([_vp, ctypes.c_char_p], _i32),
+    "shb_host_measure_class": ([_vp, _u64, _u64, _f64, ctypes.POINTER(ctypes.c_uint32), _P64, _PF64], _i32),
     "shb_host_seqsum_const": ([_f64, _u64], _f64),
     "shb_host_pairwise_sum_const": ([_f64, _u64], _f64),
 }
@@ -87,6 +103,8 @@ def check(rc: int, what: str = "") -> None:
         raise ValueError(text)
     if rc == SHB_ENOMEM:
         raise MemoryError(text)
+    if rc == SHB_EIO:
+        raise OSError(text)
     raise RuntimeError(text)
 
 

@@ -270,6 +270,57 @@ double shb_host_pairwise_sum_const(double w, uint64_t count)
     return p.run(count);
 }
 
+int shb_host_measure_class(const uint64_t *counts, uint64_t ncls, uint64_t q, double u, uint32_t *k_out,
+                           uint64_t *M_out, double *amp_out)
+{
+    if (!counts || !k_out || !M_out || !amp_out) return set_error(SHB_EINVAL, "null argument");
+    if (q < 2 || (q & (q - 1))) return set_error(SHB_EINVAL, "q must be a power of two >= 2");
+    uint64_t nclasses = ncls;
+    while (nclasses > 0 && counts[nclasses - 1] == 0) nclasses--;
+    if (nclasses == 0) return set_error(SHB_EINVAL, "all class counts are zero");
+    if (nclasses - 1 > 0xFFFFFFFFull) return set_error(SHB_EINVAL, "residue class exceeds 32 bits");
+    // init_uniform's amplitude (qstate.py:59) and its weight np.abs(a)**2 (qstate.py:95)
+    const double a = 1.0 / sqrt((double)q);
+    const double w0 = a * a;
+    // bincount (qstate.py:97) per bin, then np.cumsum (qstate.py:98): both sequential
+    double cum = 0.0, total = 0.0;
+    {
+        std::map<uint64_t, double> memo;
+        for (uint64_t v = 0; v < nclasses; v++) {
+            const uint64_t c = counts[v];
+            if (c == 0) continue;
+            auto it = memo.find(c);
+            const double p = it != memo.end() ? it->second : (memo[c] = seqsum_const_impl(w0, c));
+            total = total + p;
+        }
+    }
+    // searchsorted(cum, u * cum[-1], side="right") (qstate.py:99), clamped (qstate.py:100)
+    const double target = u * total;
+    uint64_t k = 0;
+    {
+        std::map<uint64_t, double> memo;
+        for (k = 0; k < nclasses; k++) {
+            const uint64_t c = counts[k];
+            if (c) {
+                auto it = memo.find(c);
+                const double p = it != memo.end() ? it->second : (memo[c] = seqsum_const_impl(w0, c));
+                cum = cum + p;
+            }
+            if (cum > target) break;
+        }
+    }
+    if (k > nclasses - 1) k = nclasses - 1;
+    const uint64_t M = counts[k];
+    // kept = sqrt(weights[mask].sum()) (pairwise, qstate.py:102); amplitude / kept is a
+    // complex / complex division in numpy: Smith's form, (a + 0*rat) * (1 / kept)
+    PairwiseConst pw{w0, {}};
+    const double kept = sqrt(pw.run(M));
+    *k_out = (uint32_t)k;
+    *M_out = M;
+    *amp_out = a * (1.0 / kept);
+    return SHB_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Host-buffer drop-ins: the C-level form of qft.dense_dft / tiled_dft and of
 // the _kernels.partial_row_sums seam.  Device memory is stream-ordered and

@@ -1,5 +1,5 @@
 // Stage 3 of the hot path: the QFT as a direct DFT over the collapsed support
-// (qft.dense_dft / qft.tiled_dft, qft.py:270-317; inner loop
+// (qft.dense_dft / qft.tiled_dft, qft.py:95-142; inner loop
 // _kernels.partial_row_sums, _kernels.py:16-30).
 //
 //   V_c = scale * sum_j amp_j * e^{+2 pi i (a0 + j*stride) c / q}

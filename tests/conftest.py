@@ -29,12 +29,12 @@ def cuda_available() -> bool:
         return False
 
 
-def build_c_demo(tmp_path):
-    """Compile examples/c_abi_demo.c against include/shorb200.h + libshorb200.so."""
+def build_c_demo(tmp_path, name: str = "c_abi_demo"):
+    """Compile examples/<name>.c against include/shorb200.h + libshorb200.so."""
     import subprocess
     pkg = ROOT / "paper_1801_01434_b200"
-    exe = tmp_path / "c_abi_demo"
-    cmd = ["gcc", "-O2", "-I", str(ROOT / "include"), str(ROOT / "examples" / "c_abi_demo.c"),
+    exe = tmp_path / name
+    cmd = ["gcc", "-O2", "-Wall", "-I", str(ROOT / "include"), str(ROOT / "examples" / f"{name}.c"),
            "-L", str(pkg), f"-Wl,-rpath,{pkg}", "-l:libshorb200.so", "-lm", "-o", str(exe)]
     subprocess.run(cmd, check=True, capture_output=True)
     return exe
