@@ -384,10 +384,13 @@ static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t s
 // m8n8k4.f64 fragments: A[r = lane/4][k = lane%4], B[k = lane%4][n = lane/4],
 // C/D[r = lane/4][n = 2*(lane%4) + {0,1}].
 #ifndef SHB_MMA_B
-#define SHB_MMA_B 32
+#define SHB_MMA_B 64
 #endif
 #ifndef SHB_MMA_CT
-#define SHB_MMA_CT 2
+#define SHB_MMA_CT 1
+#endif
+#ifndef SHB_MMA_MINB
+#define SHB_MMA_MINB 1
 #endif
 constexpr int MMA_B = SHB_MMA_B;           // k extent per block row
 constexpr int MMA_KS = MMA_B / 4;          // k-steps of 4
@@ -398,11 +401,14 @@ constexpr int MMA_OUT_PER_CTA = MMA_WARPS * MMA_CT * 8;  // 128
 constexpr int MMA_SEG_BLOCKS = 8192 / MMA_BLOCK;  // exact re-seed every 8192 amplitudes
 constexpr int MMA_CHUNK = 1024;            // amplitudes per smem stage (4 blocks)
 
+// Not volatile: the compiler may schedule independent DMMAs between the two
+// that feed one accumulator (a volatile asm keeps program order, and each
+// dependent pair then stalls for the full DMMA latency).
 __device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b)
 {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d0), "+d"(d1)
-                 : "d"(a), "d"(b));
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
 }
 
 struct MmaArgs {
@@ -419,7 +425,7 @@ struct MmaArgs {
 };
 
 template <bool UNIF>
-__global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1)
+__global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, SHB_MMA_MINB)
     dft_mma_kernel(const MmaArgs p)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -489,6 +495,7 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1
         }
     }
 
+    const double amp_r = p.amp_re, amp_i = p.amp_im;
     uint64_t seg_blocks = 0;
     for (uint64_t jb = 0; consumer && jb < nblocks; jb++) {
         const uint64_t ch = jb / (MMA_CHUNK / MMA_BLOCK);
@@ -497,29 +504,50 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, 1
         if (!UNIF && boff == 0) mbar_wait(&full_bar[s], (uint32_t)(ch / DFT_STAGES) & 1u);
         const double2 *sb = buf + (size_t)s * MMA_CHUNK + boff;
         const uint64_t jblk = jb * MMA_BLOCK;
+        // T = A * G (complex): Re += ar*gr - ai*gi ; Im += ar*gi + ai*gr, issued
+        // so that 2*MMA_CT independent DMMAs separate the two updates of each
+        // accumulator
+        auto mma_step = [&](int ks, double ar, double ai) {
 #pragma unroll
-        for (int ks = 0; ks < MMA_KS; ks++) {
-            const int jl = r * MMA_B + ks * 4 + kq;  // A fragment: row j1 = r, col k
-            double ar, ai;
-            if (jblk + jl < p.length) {
-                if (UNIF) {
-                    ar = p.amp_re;
-                    ai = p.amp_im;
-                } else {
-                    const double2 av = sb[jl];
-                    ar = av.x;
-                    ai = av.y;
-                }
-            } else {
-                ar = ai = 0.0;  // ragged tail
+            for (int ct = 0; ct < MMA_CT; ct++) {
+                dmma_8x8x4(dr[ct][0], dr[ct][1], ar, gr[ct][ks]);
+                dmma_8x8x4(di[ct][0], di[ct][1], ar, gi[ct][ks]);
             }
 #pragma unroll
             for (int ct = 0; ct < MMA_CT; ct++) {
-                // T = A * G (complex): Re += ar*gr - ai*gi ; Im += ar*gi + ai*gr
-                dmma_8x8x4(dr[ct][0], dr[ct][1], ar, gr[ct][ks]);
                 dmma_8x8x4(dr[ct][0], dr[ct][1], -ai, gi[ct][ks]);
-                dmma_8x8x4(di[ct][0], di[ct][1], ar, gi[ct][ks]);
                 dmma_8x8x4(di[ct][0], di[ct][1], ai, gr[ct][ks]);
+            }
+        };
+        // A fragment: row j1 = r, col k of the block.  Only the last block can
+        // be ragged; full blocks take the operands without a bounds select (a
+        // per-step select rewrites the A register the previous DMMAs read).
+        if (jblk + MMA_BLOCK <= p.length) {
+#pragma unroll
+            for (int ks = 0; ks < MMA_KS; ks++) {
+                if (UNIF) {
+                    mma_step(ks, amp_r, amp_i);
+                } else {
+                    const double2 av = sb[r * MMA_B + ks * 4 + kq];
+                    mma_step(ks, av.x, av.y);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int ks = 0; ks < MMA_KS; ks++) {
+                const int jl = r * MMA_B + ks * 4 + kq;
+                double ar = 0.0, ai = 0.0;  // ragged tail: zero rows
+                if (jblk + jl < p.length) {
+                    if (UNIF) {
+                        ar = amp_r;
+                        ai = amp_i;
+                    } else {
+                        const double2 av = sb[jl];
+                        ar = av.x;
+                        ai = av.y;
+                    }
+                }
+                mma_step(ks, ar, ai);
             }
         }
         if (!UNIF && (boff + MMA_BLOCK == MMA_CHUNK || jb + 1 == nblocks)) {
