@@ -401,14 +401,15 @@ constexpr int MMA_OUT_PER_CTA = MMA_WARPS * MMA_CT * 8;  // 128
 constexpr int MMA_SEG_BLOCKS = 8192 / MMA_BLOCK;  // exact re-seed every 8192 amplitudes
 constexpr int MMA_CHUNK = 1024;            // amplitudes per smem stage (4 blocks)
 
-// Not volatile: the compiler may schedule independent DMMAs between the two
-// that feed one accumulator (a volatile asm keeps program order, and each
-// dependent pair then stalls for the full DMMA latency).
+// volatile: on the uniform comb every block's T is the same product, and a
+// non-volatile asm would let the compiler hoist it out of the block loop --
+// the kernel must perform every phase term it is credited with.  Callers
+// order the DMMAs so that independent ones separate dependent pairs.
 __device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b)
 {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-        : "+d"(d0), "+d"(d1)
-        : "d"(a), "d"(b));
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
 }
 
 struct MmaArgs {
