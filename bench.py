@@ -302,7 +302,12 @@ def run_b200(args):
     clk_mhz = clk.get("sm_mhz") or 1965.0
     peak_tf = sms * 64 * 2 * clk_mhz * 1e6 / 1e12
     dft_s = statistics.mean(dft_ms) / 1000.0
-    achieved_tf = 8.0 * rec.phase_terms / dft_s / 1e12
+    # the kernel the attempt launched (uniform comb) and its flops per phase term:
+    # 4 in the real-A DMMA form (amp*cos, amp*sin), 8 for a complex multiply-add
+    fpt = ctypes_int()
+    kname = lib.shb_dft_engine(1, 1, q, nat.FP64 if args.precision == "fp64" else nat.FP32, 1, fpt)
+    kname = kname.decode() if kname else "dft"
+    achieved_tf = fpt.value * rec.phase_terms / dft_s / 1e12
     # DRAM bytes per DFT launch from the committed ncu --set full capture, only
     # when that capture was taken at this very configuration
     prof = ROOT / "profiles" / "dft_traffic.json"
@@ -321,12 +326,12 @@ def run_b200(args):
     roof = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
             "frac": achieved_tf / peak_tf, "traffic": traffic, "traffic_note": traffic_note,
             "traffic_unit": "bytes/launch", "algorithmic_bytes_per_launch": 24 * (q // world),
-            "peak_source": f"nominal FP64: {sms} SMs x 64 DFMA/clk x 2 flops x {clk_mhz:.0f} MHz "
+            "peak_source": f"nominal FP64 (one datapath for DFMA and DMMA): {sms} SMs x 64 FMA/clk x 2 flops x {clk_mhz:.0f} MHz "
                            "(median SM clock in the timed region); MEASURED_PEAKS.json has no FP64 figure",
             "peak_probe": ptf.value,
             "peak_probe_note": "shb_fp64_peak: independent DFMA chains with constant operands on this GPU",
-            "kernel": "shb::dft_kernel<double>", "dft_ms_per_launch": dft_s * 1000.0,
-            "flops_per_launch": 8.0 * rec.phase_terms}
+            "kernel": f"shb::{kname}", "dft_ms_per_launch": dft_s * 1000.0,
+            "flops_per_phase_term": fpt.value, "flops_per_launch": fpt.value * rec.phase_terms}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -395,6 +400,11 @@ def run_b200(args):
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def ctypes_int():
+    import ctypes
+    return ctypes.c_int(0)
 
 
 def ctypes_double():

@@ -94,6 +94,12 @@ int shb_progression_is_uniform(const double *d_amps, uint64_t length,
                                int *uniform, double *amp_re, double *amp_im,
                                void *stream);
 
+/* As shb_progression_is_uniform, plus *real = 1 if every imaginary part is
+ * zero (selects the real-amplitude DMMA form of shb_dft_real). */
+int shb_progression_kind(const double *d_amps, uint64_t length, int *uniform,
+                         int *real, double *amp_re, double *amp_im,
+                         void *stream);
+
 /* d_amps[j] = amp for j < length where the support index a0 + j*stride is in
  * d_support[0..m), 0 otherwise (collapsed register -> progression amplitudes). */
 int shb_fill_progression(const uint64_t *d_support, uint64_t m, uint64_t a0,
@@ -120,6 +126,24 @@ int shb_dft(const double *d_amps, uint64_t length, uint64_t a0,
             uint32_t tiles, double scale, int precision, double *d_out,
             double *d_prob, double *d_block_sums, void *stream);
 uint64_t shb_dft_num_blocks(uint64_t c_count, int precision);
+
+/* shb_dft for a real amplitude stream: the imaginary parts of d_amps are
+ * ignored (the caller has checked them to be zero, shb_progression_kind).
+ * FP64 with tiles == 1 runs the real-A DMMA form: 2 real products per phase
+ * term (amp*cos, amp*sin) instead of a complex multiply.  Other cases behave
+ * exactly as shb_dft. */
+int shb_dft_real(const double *d_amps, uint64_t length, uint64_t a0,
+                 uint64_t stride, uint64_t q, uint64_t c_begin,
+                 uint64_t c_count, uint32_t tiles, double scale, int precision,
+                 double *d_out, double *d_prob, double *d_block_sums,
+                 void *stream);
+
+/* Name of the kernel the three DFT entry points launch for these arguments
+ * (uniform: shb_dft_uniform; real: shb_dft_real), and the flops one phase
+ * term costs in it (*flops_per_term: 8 complex multiply-add, 4 real
+ * amplitude x complex phase).  Static string; for roofline reporting. */
+const char *shb_dft_engine(int uniform, int real, uint64_t q, int precision,
+                           uint32_t tiles, int *flops_per_term);
 
 /* Same transform for a uniform comb: every one of the `length` progression
  * amplitudes equals (amp_re + i amp_im) -- the collapsed register of

@@ -37,8 +37,12 @@ SIGNATURES = {
     "shb_state_progression": ([_vp, _u64, _P64, _P64, _P64, _vp], _i32),
     "shb_gather_progression": ([_vp, _u64, _u64, _u64, _vp, _vp], _i32),
     "shb_progression_is_uniform": ([_vp, _u64, ctypes.POINTER(ctypes.c_int), _PF64, _PF64, _vp], _i32),
+    "shb_progression_kind": ([_vp, _u64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), _PF64, _PF64,
+                              _vp], _i32),
     "shb_fill_progression": ([_vp, _u64, _u64, _u64, _u64, _f64, _f64, _vp, _vp], _i32),
     "shb_dft": ([_vp, _u64, _u64, _u64, _u64, _u64, _u64, _u32, _f64, _i32, _vp, _vp, _vp, _vp], _i32),
+    "shb_dft_engine": ([ctypes.c_int, ctypes.c_int, _u64, _i32, _u32, ctypes.POINTER(ctypes.c_int)], ctypes.c_char_p),
+    "shb_dft_real": ([_vp, _u64, _u64, _u64, _u64, _u64, _u64, _u32, _f64, _i32, _vp, _vp, _vp, _vp], _i32),
     "shb_dft_uniform": ([_f64, _f64, _u64, _u64, _u64, _u64, _u64, _u64, _u32, _f64, _i32, _vp, _vp, _vp, _vp],
                         _i32),
     "shb_dft_num_blocks": ([_u64, _i32], _u64),

@@ -349,9 +349,9 @@ static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t i
         SHB_TRY(scratch_alloc(d_out, c_count * 16, st));
         // data-selected kernel: a uniform comb (e.g. a collapsed register) takes the
         // constant-operand path, anything else the TMA-staged amplitude stream
-        int uni = 0;
+        int uni = 0, real = 0;
         double ur = 0.0, ui = 0.0;
-        if (len) SHB_TRY(shb_progression_is_uniform((const double *)d_amps.ptr, len, &uni, &ur, &ui, st));
+        if (len) SHB_TRY(shb_progression_kind((const double *)d_amps.ptr, len, &uni, &real, &ur, &ui, st));
         // output slices: slice i's D2H copy (second stream) overlaps slice i+1's
         // DFT.  Outputs are independent sums, so slicing changes no value.
         const int nslice = c_count >= (1ull << 22) ? 8 : 1;
@@ -374,8 +374,9 @@ static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t i
                 rc = shb_dft_uniform(ur, ui, len, a0 + index_base, stride, q, c_begin + lo, hi - lo, tiles,
                                      scale, precision, dout + 2 * lo, nullptr, nullptr, st);
             else
-                rc = shb_dft((const double *)d_amps.ptr, len, a0 + index_base, stride, q, c_begin + lo, hi - lo,
-                             tiles, scale, precision, dout + 2 * lo, nullptr, nullptr, st);
+                rc = (real ? shb_dft_real : shb_dft)((const double *)d_amps.ptr, len, a0 + index_base, stride, q,
+                                                     c_begin + lo, hi - lo, tiles, scale, precision, dout + 2 * lo,
+                                                     nullptr, nullptr, st);
             if (rc != SHB_OK) break;
             SHB_TRY_CUDA(cudaEventRecord(ev[i], st));
             SHB_TRY_CUDA(cudaStreamWaitEvent(cp, ev[i], 0));

@@ -233,14 +233,16 @@ __global__ void uniform_check_kernel(const double2 *__restrict__ amps, uint64_t 
 {
     const double2 a0 = amps[0];
     const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
-    bool d = false;
+    bool d = false, cplx = false;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += step) {
         const double2 v = amps[j];
         // bitwise comparison: -0.0 and +0.0 or NaN payloads are not "equal"
         d |= (__double_as_longlong(v.x) != __double_as_longlong(a0.x)) ||
              (__double_as_longlong(v.y) != __double_as_longlong(a0.y));
+        cplx |= !(v.y == 0.0);  // bit 1: some imaginary part is nonzero (or NaN)
     }
-    if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(diff, 1u);
+    const bool bd = __syncthreads_or(d), bc = __syncthreads_or(cplx);
+    if (threadIdx.x == 0 && (bd || bc)) atomicOr(diff, (bd ? 1u : 0u) | (bc ? 2u : 0u));
 }
 
 static unsigned grid_for(uint64_t n, int threads, int per_sm)
@@ -343,11 +345,12 @@ extern "C" int shb_gather_progression(const double *d_state, uint64_t a0, uint64
     return SHB_OK;
 }
 
-extern "C" int shb_progression_is_uniform(const double *d_amps, uint64_t length, int *uniform, double *amp_re,
-                                          double *amp_im, void *stream)
+extern "C" int shb_progression_kind(const double *d_amps, uint64_t length, int *uniform, int *real,
+                                    double *amp_re, double *amp_im, void *stream)
 {
     if (!uniform) return set_error(SHB_EINVAL, "null output");
     *uniform = 0;
+    if (real) *real = 1;
     if (length == 0) return SHB_OK;
     cudaStream_t st = as_stream(stream);
     Scratch diff;
@@ -362,10 +365,17 @@ extern "C" int shb_progression_is_uniform(const double *d_amps, uint64_t length,
     SHB_TRY_CUDA(cudaMemcpyAsync(&h, diff.ptr, sizeof h, cudaMemcpyDeviceToHost, st));
     SHB_TRY_CUDA(cudaMemcpyAsync(a, d_amps, sizeof a, cudaMemcpyDeviceToHost, st));
     SHB_TRY_CUDA(cudaStreamSynchronize(st));
-    *uniform = h ? 0 : 1;
+    *uniform = (h & 1u) ? 0 : 1;
+    if (real) *real = (h & 2u) ? 0 : 1;
     if (amp_re) *amp_re = a[0];
     if (amp_im) *amp_im = a[1];
     return SHB_OK;
+}
+
+extern "C" int shb_progression_is_uniform(const double *d_amps, uint64_t length, int *uniform, double *amp_re,
+                                          double *amp_im, void *stream)
+{
+    return shb_progression_kind(d_amps, length, uniform, nullptr, amp_re, amp_im, stream);
 }
 
 extern "C" int shb_fill_progression(const uint64_t *d_support, uint64_t m, uint64_t a0, uint64_t stride,

@@ -384,7 +384,10 @@ static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t s
 // m8n8k4.f64 fragments: A[r = lane/4][k = lane%4], B[k = lane%4][n = lane/4],
 // C/D[r = lane/4][n = 2*(lane%4) + {0,1}].
 #ifndef SHB_MMA_B
-#define SHB_MMA_B 64
+#define SHB_MMA_B 64    // generic amplitude stream (register cap 168 with the producer warp)
+#endif
+#ifndef SHB_MMA_BU
+#define SHB_MMA_BU 128  // uniform comb (no amplitude registers: G takes 128 of them)
 #endif
 #ifndef SHB_MMA_CT
 #define SHB_MMA_CT 1
@@ -392,14 +395,22 @@ static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t s
 #ifndef SHB_MMA_MINB
 #define SHB_MMA_MINB 1
 #endif
-constexpr int MMA_B = SHB_MMA_B;           // k extent per block row
-constexpr int MMA_KS = MMA_B / 4;          // k-steps of 4
-constexpr int MMA_BLOCK = 8 * MMA_B;       // amplitudes per block (256)
 constexpr int MMA_CT = SHB_MMA_CT;         // 8-output tiles per warp
 constexpr int MMA_WARPS = 8;               // consumer warps
-constexpr int MMA_OUT_PER_CTA = MMA_WARPS * MMA_CT * 8;  // 128
-constexpr int MMA_SEG_BLOCKS = 8192 / MMA_BLOCK;  // exact re-seed every 8192 amplitudes
-constexpr int MMA_CHUNK = 1024;            // amplitudes per smem stage (4 blocks)
+constexpr int MMA_OUT_PER_CTA = MMA_WARPS * MMA_CT * 8;  // 64
+#ifndef SHB_MMA_NACC
+#define SHB_MMA_NACC 1  // accumulator sets by k-step parity (real form)
+#endif
+#ifndef SHB_MMA_PIPE
+#define SHB_MMA_PIPE 0  // 2-set software pipeline over blocks
+#endif
+#ifndef SHB_MMA_GREC
+#define SHB_MMA_GREC 1  // G fragments by recurrence from 2 exact phases
+#endif
+#ifndef SHB_MMA_SEG
+#define SHB_MMA_SEG 32768  // amplitudes between exact per-lane re-seeds
+#endif
+constexpr int MMA_CHUNK = 1024;            // amplitudes per smem stage (generic path)
 
 // volatile: on the uniform comb every block's T is the same product, and a
 // non-volatile asm would let the compiler hoist it out of the block loop --
@@ -425,10 +436,24 @@ struct MmaArgs {
     double *block_sums;
 };
 
-template <bool UNIF>
+// REALA: every amplitude is real (always so on the uniform path, where the
+// amplitude is factored out and A = 1).  A real A times the complex G is two
+// real GEMMs (Re T = A Gr, Im T = A Gi): 2 DMMAs per k-step instead of 4, i.e.
+// 4 flops per phase term -- the multiplies by Im A = 0 are not issued.  The two
+// DMMA chains alternate between two accumulator sets by k-step parity so that
+// dependent DMMAs on one accumulator are 4 instructions apart.
+template <bool UNIF, bool REALA>
 __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, SHB_MMA_MINB)
     dft_mma_kernel(const MmaArgs p)
 {
+    constexpr int MMA_B = UNIF ? SHB_MMA_BU : SHB_MMA_B;  // k extent per block row
+    constexpr int MMA_KS = MMA_B / 4;                      // k-steps of 4
+    constexpr int MMA_BLOCK = 8 * MMA_B;                   // amplitudes per block
+    constexpr int MMA_SEG_BLOCKS = SHB_MMA_SEG / MMA_BLOCK > 0 ? SHB_MMA_SEG / MMA_BLOCK : 1;
+    constexpr int BPC = MMA_CHUNK / MMA_BLOCK > 0 ? MMA_CHUNK / MMA_BLOCK : 1;  // blocks per smem stage
+    static_assert(UNIF || MMA_CHUNK % MMA_BLOCK == 0, "smem stages must hold whole blocks");
+    constexpr int NACC = REALA ? SHB_MMA_NACC : 1;
+    constexpr int NP = SHB_MMA_PIPE ? 2 : 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *buf = reinterpret_cast<double2 *>(smem_raw);
     __shared__ __align__(8) uint64_t full_bar[DFT_STAGES];
@@ -471,18 +496,31 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, S
     double ur[MMA_CT][2], ui[MMA_CT][2];       // U = w^{-8B} for the D columns
     double hr[MMA_CT][2], hi[MMA_CT][2];       // per-lane Horner over blocks (this segment)
     double vr[MMA_CT][2], vi[MMA_CT][2];       // per-lane totals
-    double dr[MMA_CT][2], di[MMA_CT][2];       // MMA accumulators (Re T, Im T)
+    double dr[NP][NACC][MMA_CT][2], di[NP][NACC][MMA_CT][2];  // MMA accumulators (Re T, Im T)
 #pragma unroll
     for (int ct = 0; ct < MMA_CT; ct++) {
         const uint64_t tile = cta_c + (uint64_t)warp * (MMA_CT * 8) + ct * 8;
         cG[ct] = p.c_begin + tile + r;
+        if (SHB_MMA_GREC) {
+            // G[ks] = w^{4 ks + kq}: two exact sincospi and 15 complex products
+            // (<= ~15 ulp; the same G serves every block of the transform)
+            double sr, si4;
+            phase((4 * p.stride * cG[ct]) & qmask, q, p.two_over_q, sr, si4);
+            phase(((uint64_t)kq * p.stride * cG[ct]) & qmask, q, p.two_over_q, gr[ct][0], gi[ct][0]);
 #pragma unroll
-        for (int ks = 0; ks < MMA_KS; ks++) {
-            const uint64_t k = (uint64_t)ks * 4 + kq;
-            double co, si;
-            phase((k * p.stride * cG[ct]) & qmask, q, p.two_over_q, co, si);
-            gr[ct][ks] = co;
-            gi[ct][ks] = si;
+            for (int ks = 1; ks < MMA_KS; ks++) {
+                gr[ct][ks] = fma(gr[ct][ks - 1], sr, -gi[ct][ks - 1] * si4);
+                gi[ct][ks] = fma(gr[ct][ks - 1], si4, gi[ct][ks - 1] * sr);
+            }
+        } else {
+#pragma unroll
+            for (int ks = 0; ks < MMA_KS; ks++) {
+                const uint64_t k = (uint64_t)ks * 4 + kq;
+                double co, si;
+                phase((k * p.stride * cG[ct]) & qmask, q, p.two_over_q, co, si);
+                gr[ct][ks] = co;
+                gi[ct][ks] = si;
+            }
         }
 #pragma unroll
         for (int h = 0; h < 2; h++) {
@@ -492,94 +530,123 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, S
             ur[ct][h] = co;
             ui[ct][h] = -si;  // w^{-8B}
             hr[ct][h] = hi[ct][h] = vr[ct][h] = vi[ct][h] = 0.0;
-            dr[ct][h] = di[ct][h] = 0.0;
+#pragma unroll
+            for (int s = 0; s < NP * NACC; s++) dr[s / NACC][s % NACC][ct][h] = di[s / NACC][s % NACC][ct][h] = 0.0;
         }
     }
 
     const double amp_r = p.amp_re, amp_i = p.amp_im;
-    uint64_t seg_blocks = 0;
-    for (uint64_t jb = 0; consumer && jb < nblocks; jb++) {
-        const uint64_t ch = jb / (MMA_CHUNK / MMA_BLOCK);
-        const int s = (int)(ch % DFT_STAGES);
-        const int boff = (int)(jb % (MMA_CHUNK / MMA_BLOCK)) * MMA_BLOCK;
-        if (!UNIF && boff == 0) mbar_wait(&full_bar[s], (uint32_t)(ch / DFT_STAGES) & 1u);
-        const double2 *sb = buf + (size_t)s * MMA_CHUNK + boff;
-        const uint64_t jblk = jb * MMA_BLOCK;
-        // T = A * G (complex): Re += ar*gr - ai*gi ; Im += ar*gi + ai*gr, issued
-        // so that 2*MMA_CT independent DMMAs separate the two updates of each
-        // accumulator
-        auto mma_step = [&](int ks, double ar, double ai) {
+    // Software pipeline over blocks (NP = 2 accumulator sets): iteration jb
+    // issues block jb's DMMAs into set jb&1, then folds block jb-1 from the
+    // other set, so the fold (which waits on the last DMMA of its block) sits
+    // behind a block of independent DMMAs instead of draining the tensor pipe.
+    // Warps of a CTA run in lockstep, so without this every warp drained at
+    // the same time (ncu: DADD of the fold = 21% of stall samples).
+    for (uint64_t i = 0; consumer && i <= nblocks; i += NP) {
 #pragma unroll
-            for (int ct = 0; ct < MMA_CT; ct++) {
-                dmma_8x8x4(dr[ct][0], dr[ct][1], ar, gr[ct][ks]);
-                dmma_8x8x4(di[ct][0], di[ct][1], ar, gi[ct][ks]);
-            }
+        for (int P = 0; P < NP; P++) {
+            const uint64_t jb = i + P;
+            if (jb < nblocks) {
+                const uint64_t ch = jb / BPC;
+                const int s = (int)(ch % DFT_STAGES);
+                const int boff = (int)(jb % BPC) * MMA_BLOCK;
+                if (!UNIF && boff == 0) mbar_wait(&full_bar[s], (uint32_t)(ch / DFT_STAGES) & 1u);
+                const double2 *sb = buf + (size_t)s * MMA_CHUNK + boff;
+                const uint64_t jblk = jb * MMA_BLOCK;
+                // T = A * G (complex): Re += ar*gr - ai*gi ; Im += ar*gi + ai*gr, issued
+                // so that independent DMMAs separate the updates of each accumulator
+                auto mma_step = [&](int ks, double ar, double ai) {
+                    if (REALA) {
+                        const int sa = ks % NACC;
 #pragma unroll
-            for (int ct = 0; ct < MMA_CT; ct++) {
-                dmma_8x8x4(dr[ct][0], dr[ct][1], -ai, gi[ct][ks]);
-                dmma_8x8x4(di[ct][0], di[ct][1], ai, gr[ct][ks]);
-            }
-        };
-        // A fragment: row j1 = r, col k of the block.  Only the last block can
-        // be ragged; full blocks take the operands without a bounds select (a
-        // per-step select rewrites the A register the previous DMMAs read).
-        if (jblk + MMA_BLOCK <= p.length) {
+                        for (int ct = 0; ct < MMA_CT; ct++) {
+                            dmma_8x8x4(dr[P][sa][ct][0], dr[P][sa][ct][1], ar, gr[ct][ks]);
+                            dmma_8x8x4(di[P][sa][ct][0], di[P][sa][ct][1], ar, gi[ct][ks]);
+                        }
+                        return;
+                    }
 #pragma unroll
-            for (int ks = 0; ks < MMA_KS; ks++) {
-                if (UNIF) {
-                    mma_step(ks, amp_r, amp_i);
+                    for (int ct = 0; ct < MMA_CT; ct++) {
+                        dmma_8x8x4(dr[P][0][ct][0], dr[P][0][ct][1], ar, gr[ct][ks]);
+                        dmma_8x8x4(di[P][0][ct][0], di[P][0][ct][1], ar, gi[ct][ks]);
+                    }
+#pragma unroll
+                    for (int ct = 0; ct < MMA_CT; ct++) {
+                        dmma_8x8x4(dr[P][0][ct][0], dr[P][0][ct][1], -ai, gi[ct][ks]);
+                        dmma_8x8x4(di[P][0][ct][0], di[P][0][ct][1], ai, gr[ct][ks]);
+                    }
+                };
+                // A fragment: row j1 = r, col k of the block.  Only the last block can
+                // be ragged; full blocks take the operands without a bounds select (a
+                // per-step select rewrites the A register the previous DMMAs read).
+                if (jblk + MMA_BLOCK <= p.length) {
+#pragma unroll
+                    for (int ks = 0; ks < MMA_KS; ks++) {
+                        if (UNIF) {
+                            mma_step(ks, amp_r, amp_i);
+                        } else if (REALA) {
+                            mma_step(ks, sb[r * MMA_B + ks * 4 + kq].x, 0.0);
+                        } else {
+                            const double2 av = sb[r * MMA_B + ks * 4 + kq];
+                            mma_step(ks, av.x, av.y);
+                        }
+                    }
                 } else {
-                    const double2 av = sb[r * MMA_B + ks * 4 + kq];
-                    mma_step(ks, av.x, av.y);
-                }
-            }
-        } else {
 #pragma unroll
-            for (int ks = 0; ks < MMA_KS; ks++) {
-                const int jl = r * MMA_B + ks * 4 + kq;
-                double ar = 0.0, ai = 0.0;  // ragged tail: zero rows
-                if (jblk + jl < p.length) {
-                    if (UNIF) {
-                        ar = amp_r;
-                        ai = amp_i;
-                    } else {
-                        const double2 av = sb[jl];
-                        ar = av.x;
-                        ai = av.y;
+                    for (int ks = 0; ks < MMA_KS; ks++) {
+                        const int jl = r * MMA_B + ks * 4 + kq;
+                        double ar = 0.0, ai = 0.0;  // ragged tail: zero rows
+                        if (jblk + jl < p.length) {
+                            if (UNIF) {
+                                ar = amp_r;
+                                ai = amp_i;
+                            } else {
+                                const double2 av = sb[jl];
+                                ar = av.x;
+                                ai = av.y;
+                            }
+                        }
+                        mma_step(ks, ar, ai);
                     }
                 }
-                mma_step(ks, ar, ai);
-            }
-        }
-        if (!UNIF && (boff + MMA_BLOCK == MMA_CHUNK || jb + 1 == nblocks)) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[s]);
-        }
-        // Horner over blocks: h = h * w^{-8B} + T ; T reset
-#pragma unroll
-        for (int ct = 0; ct < MMA_CT; ct++)
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const double nr = fma(hr[ct][h], ur[ct][h], fma(-hi[ct][h], ui[ct][h], dr[ct][h]));
-                const double ni = fma(hr[ct][h], ui[ct][h], fma(hi[ct][h], ur[ct][h], di[ct][h]));
-                hr[ct][h] = nr;
-                hi[ct][h] = ni;
-                dr[ct][h] = di[ct][h] = 0.0;
-            }
-        if (++seg_blocks == MMA_SEG_BLOCKS || jb + 1 == nblocks) {
-            // exact seed of this lane's last row: a0 + (8B jb + B r) * stride
-            const uint64_t a_lane = p.a0 + (jb * MMA_BLOCK + (uint64_t)r * MMA_B) * p.stride;
-#pragma unroll
-            for (int ct = 0; ct < MMA_CT; ct++)
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    double sc, ss;
-                    phase((a_lane * cD[ct][h]) & qmask, q, p.two_over_q, sc, ss);
-                    vr[ct][h] = fma(sc, hr[ct][h], fma(-ss, hi[ct][h], vr[ct][h]));
-                    vi[ct][h] = fma(sc, hi[ct][h], fma(ss, hr[ct][h], vi[ct][h]));
-                    hr[ct][h] = hi[ct][h] = 0.0;
+                if (!UNIF && (boff + MMA_BLOCK == MMA_CHUNK || jb + 1 == nblocks)) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty_bar[s]);
                 }
-            seg_blocks = 0;
+            }
+            // fold block jf = jb - (NP - 1) from set Q
+            const int Q = (P + 1) % NP;  // constant after unrolling
+            if (jb + 1 >= (uint64_t)NP && jb + 1 - NP < nblocks) {
+                const uint64_t jf = jb + 1 - NP;
+                // Horner over blocks: h = h * w^{-8B} + T ; T reset
+#pragma unroll
+                for (int ct = 0; ct < MMA_CT; ct++)
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const double tr_ = NACC > 1 ? dr[Q][0][ct][h] + dr[Q][NACC - 1][ct][h] : dr[Q][0][ct][h];
+                        const double ti_ = NACC > 1 ? di[Q][0][ct][h] + di[Q][NACC - 1][ct][h] : di[Q][0][ct][h];
+                        const double nr = fma(hr[ct][h], ur[ct][h], fma(-hi[ct][h], ui[ct][h], tr_));
+                        const double ni = fma(hr[ct][h], ui[ct][h], fma(hi[ct][h], ur[ct][h], ti_));
+                        hr[ct][h] = nr;
+                        hi[ct][h] = ni;
+#pragma unroll
+                        for (int s2 = 0; s2 < NACC; s2++) dr[Q][s2][ct][h] = di[Q][s2][ct][h] = 0.0;
+                    }
+                if ((jf + 1) % MMA_SEG_BLOCKS == 0 || jf + 1 == nblocks) {
+                    // exact seed of this lane's last row: a0 + (8B jf + B r) * stride
+                    const uint64_t a_lane = p.a0 + (jf * MMA_BLOCK + (uint64_t)r * MMA_B) * p.stride;
+#pragma unroll
+                    for (int ct = 0; ct < MMA_CT; ct++)
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            double sc, ss;
+                            phase((a_lane * cD[ct][h]) & qmask, q, p.two_over_q, sc, ss);
+                            vr[ct][h] = fma(sc, hr[ct][h], fma(-ss, hi[ct][h], vr[ct][h]));
+                            vi[ct][h] = fma(sc, hi[ct][h], fma(ss, hr[ct][h], vi[ct][h]));
+                            hr[ct][h] = hi[ct][h] = 0.0;
+                        }
+                }
+            }
         }
     }
 
@@ -637,12 +704,12 @@ __global__ void group_sums_kernel(const double *__restrict__ part, uint64_t npar
     out[g] = s;
 }
 
-template <bool UNIF>
+template <bool UNIF, bool REALA>
 static int launch_dft_mma(MmaArgs a, cudaStream_t st)
 {
     const size_t smem = UNIF ? 0 : (size_t)DFT_STAGES * MMA_CHUNK * sizeof(double2);
     if (smem)
-        SHB_TRY_CUDA(cudaFuncSetAttribute(dft_mma_kernel<UNIF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SHB_TRY_CUDA(cudaFuncSetAttribute(dft_mma_kernel<UNIF, REALA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
     const uint64_t nblk = (a.c_count + MMA_OUT_PER_CTA - 1) / MMA_OUT_PER_CTA;
     if (nblk > 0x7FFFFFFFull) return set_error(SHB_EINVAL, "too many outputs for one launch");
@@ -653,7 +720,7 @@ static int launch_dft_mma(MmaArgs a, cudaStream_t st)
         SHB_TRY(scratch_alloc(part, sizeof(double) * nblk, st));
         a.block_sums = (double *)part.ptr;
     }
-    dft_mma_kernel<UNIF><<<(unsigned)nblk, nthreads, smem, st>>>(a);
+    dft_mma_kernel<UNIF, REALA><<<(unsigned)nblk, nthreads, smem, st>>>(a);
     SHB_LAUNCHED();
     if (caller_sums) {
         constexpr int group = DFT_THREADS * Prec<double>::K / MMA_OUT_PER_CTA;
@@ -667,22 +734,30 @@ static int launch_dft_mma(MmaArgs a, cudaStream_t st)
     return SHB_OK;
 }
 
-// Engine choice for FP64, tiles == 1 (measured, profiles/r01_mma_vs_vector.json):
-// * general amplitudes: the DMMA GEMM form (27.7 vs 26.0 TF at q = 2^24; the
-//   vector form is register-file bound there);
-// * uniform comb: the vector Horner kernel (34.4 vs 32.6 TF at 2^24), except
-//   for small output ranges that its 1024-output CTAs cannot spread over 148 SMs
-//   (q = 2^16: 18.9 vs 12.1 TF) -- the DMMA form has 128 outputs per CTA.
-// SHB_DFT_ENGINE=vector|mma overrides (tests run both).
-// The choice depends on q only (not on this launch's output range), so every
-// output shard of a transform uses the same kernel and the spectrum stays
-// bitwise identical for any number of ranks.
+// Engine choice for FP64, tiles == 1 (measured, profiles/r01_mma_real.json):
+// * uniform comb and real amplitudes: the real-A DMMA form, 2 real products
+//   per phase term (7.7-8.0e12 terms/s at q = 2^24 and 2^30, vs 4.3e12 for the
+//   vector Horner kernel, whose complex recurrence needs 4 FP64 ops per term
+//   whatever the amplitudes);
+// * complex amplitudes: the complex DMMA form (30 vs 26 TF at q = 2^24; the
+//   vector form is register-file bound there).
+// The vector kernel serves tiles > 1 and FP32.  SHB_DFT_ENGINE=vector|mma
+// overrides (tests run both).  The choice does not depend on this launch's
+// output range, so every output shard of a transform uses the same kernel and
+// the spectrum stays bitwise identical for any number of ranks.
 static bool use_mma_engine(bool uniform, uint64_t q)
 {
+    (void)uniform;
+    (void)q;
     const char *e = getenv("SHB_DFT_ENGINE");
     if (e && e[0]) return e[0] == 'm';
-    if (!uniform) return true;
-    return q < (1ull << 21);  // below ~1.2M outputs the vector CTAs cannot fill 148 SMs
+    return true;
+}
+
+static bool use_real_form()
+{
+    const char *rf = getenv("SHB_MMA_REAL");
+    return !(rf && rf[0] == '0');
 }
 
 static int validate(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin,
@@ -744,9 +819,27 @@ extern "C" int shb_dft(const double *d_amps, uint64_t length, uint64_t a0, uint6
     if (tiles == 1 && length && use_mma_engine(false, q)) {
         MmaArgs m{(const double2 *)d_amps, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
                   0.0, 0.0, scale, 0.0, (double2 *)d_out, d_prob, d_block_sums};
-        return launch_dft_mma<false>(m, st);
+        return launch_dft_mma<false, false>(m, st);
     }
     return launch_dft<double, false>(a, length, tiles, st);
+}
+
+extern "C" int shb_dft_real(const double *d_amps, uint64_t length, uint64_t a0, uint64_t stride, uint64_t q,
+                            uint64_t c_begin, uint64_t c_count, uint32_t tiles, double scale, int precision,
+                            double *d_out, double *d_prob, double *d_block_sums, void *stream)
+{
+    SHB_TRY(validate(length, a0, stride, q, c_begin, c_count, tiles, precision, d_out));
+    if (c_count == 0) return SHB_OK;
+    if (precision == SHB_FP64 && tiles == 1 && length && use_real_form() && use_mma_engine(false, q)) {
+        if (!d_amps) return set_error(SHB_EINVAL, "null amplitude buffer");
+        if (reinterpret_cast<uintptr_t>(d_amps) & 15)
+            return set_error(SHB_EINVAL, "amplitude buffer must be 16-byte aligned");
+        MmaArgs m{(const double2 *)d_amps, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
+                  0.0, 0.0, scale, 0.0, (double2 *)d_out, d_prob, d_block_sums};
+        return launch_dft_mma<false, true>(m, as_stream(stream));
+    }
+    return shb_dft(d_amps, length, a0, stride, q, c_begin, c_count, tiles, scale, precision, d_out, d_prob,
+                   d_block_sums, stream);
 }
 
 extern "C" int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, uint64_t a0, uint64_t stride,
@@ -765,7 +858,22 @@ extern "C" int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, ui
         // the amplitude is factored out (out factor = amp*scale): the MMA runs on ones
         MmaArgs m{nullptr, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
                   1.0, 0.0, a.out_re, a.out_im, (double2 *)d_out, d_prob, d_block_sums};
-        return launch_dft_mma<true>(m, st);
+        // A = 1 is real: the 2-DMMA real form (SHB_MMA_REAL=0 forces the complex form)
+        return use_real_form() ? launch_dft_mma<true, true>(m, st) : launch_dft_mma<true, false>(m, st);
     }
     return launch_dft<double, true>(a, length, tiles, st);
+}
+
+// Which kernel shb_dft / shb_dft_real / shb_dft_uniform launch for these
+// arguments, and the FP64/FP32 flops one phase term costs in it (8 for a
+// complex multiply-add, 4 for a real amplitude times a complex phase).
+extern "C" const char *shb_dft_engine(int uniform, int real, uint64_t q, int precision, uint32_t tiles,
+                                      int *flops_per_term)
+{
+    const bool mma = precision == SHB_FP64 && tiles == 1 && use_mma_engine(uniform != 0, q);
+    const bool realf = mma && (uniform || real) && use_real_form();
+    if (flops_per_term) *flops_per_term = realf ? 4 : 8;
+    if (!mma) return uniform ? "dft_kernel<uniform>" : "dft_kernel<generic>";
+    if (realf) return uniform ? "dft_mma_kernel<uniform, real A>" : "dft_mma_kernel<generic, real A>";
+    return uniform ? "dft_mma_kernel<uniform, complex A>" : "dft_mma_kernel<generic, complex A>";
 }

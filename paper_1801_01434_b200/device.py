@@ -124,6 +124,17 @@ def progression_uniform(amps, length: int):
     return complex(re.value, im.value) if u.value else None
 
 
+def progression_kind(amps, length: int):
+    """(uniform amplitude or None, all imaginary parts zero) of a progression."""
+    if length == 0:
+        return None, True
+    u, real = ctypes.c_int(0), ctypes.c_int(0)
+    re, im = ctypes.c_double(), ctypes.c_double()
+    nat.check(nat.load().shb_progression_kind(_vp(amps), length, ctypes.byref(u), ctypes.byref(real),
+                                              ctypes.byref(re), ctypes.byref(im), _stream()), "progression_kind")
+    return (complex(re.value, im.value) if u.value else None), bool(real.value)
+
+
 def fill_progression(support, m: int, a0: int, stride: int, length: int, amp: complex):
     t = _t()
     amps = t.empty(2 * max(length, 1), dtype=t.float64, device="cuda")
@@ -138,8 +149,10 @@ PRECISIONS = {"fp64": nat.FP64, "fp32": nat.FP32}
 
 def dft(amps, length: int, a0: int, stride: int, q: int, c_begin: int, c_count: int,
         tiles: int = 1, scale: float | None = None, precision: str = "fp64",
-        want_prob: bool = True):
-    """Direct DFT over a support progression; returns (out, prob, block_sums)."""
+        want_prob: bool = True, real: bool = False):
+    """Direct DFT over a support progression; returns (out, prob, block_sums).
+
+    real=True: the amplitudes' imaginary parts are zero (shb_dft_real)."""
     t = _t()
     prec = PRECISIONS[precision]
     scale = 1.0 / math.sqrt(q) if scale is None else scale
@@ -147,8 +160,9 @@ def dft(amps, length: int, a0: int, stride: int, q: int, c_begin: int, c_count: 
     prob = t.empty(max(c_count, 1), dtype=t.float64, device="cuda") if want_prob else None
     nb = int(nat.load().shb_dft_num_blocks(c_count, prec))
     bsum = t.empty(max(nb, 1), dtype=t.float64, device="cuda") if want_prob else None
-    nat.check(nat.load().shb_dft(_vp(amps), length, a0, stride, q, c_begin, c_count, tiles, scale, prec,
-                                 _vp(out), _vp(prob), _vp(bsum), _stream()), "dft")
+    fn = nat.load().shb_dft_real if real else nat.load().shb_dft
+    nat.check(fn(_vp(amps), length, a0, stride, q, c_begin, c_count, tiles, scale, prec,
+                 _vp(out), _vp(prob), _vp(bsum), _stream()), "dft")
     out = out[: 2 * c_count]
     if want_prob:
         prob, bsum = prob[:c_count], bsum[:nb]

@@ -62,8 +62,8 @@ class DeviceOps:
     def fill_progression(self, support, m, a0, stride, length, amp):
         return self.dev.fill_progression(support, m, a0, stride, length, amp)
 
-    def dft(self, amps, length, a0, stride, q, c_begin, c_count, precision):
-        return self.dev.dft(amps, length, a0, stride, q, c_begin, c_count, precision=precision)
+    def dft(self, amps, length, a0, stride, q, c_begin, c_count, precision, real=False):
+        return self.dev.dft(amps, length, a0, stride, q, c_begin, c_count, precision=precision, real=real)
 
     def dft_uniform(self, amp, length, a0, stride, q, c_begin, c_count, precision):
         return self.dev.dft_uniform(amp, length, a0, stride, q, c_begin, c_count, precision=precision)
@@ -169,7 +169,8 @@ def sharded_attempt(n: int, x: int, q: int, sampler: qstate.Sampler, *, rank: in
     if amps is None:
         out, prob, bsum = ops.dft_uniform(amp, length, a0, stride, q, c_lo, c_hi - c_lo, precision)
     else:
-        out, prob, bsum = ops.dft(amps, length, a0, stride, q, c_lo, c_hi - c_lo, precision)
+        out, prob, bsum = ops.dft(amps, length, a0, stride, q, c_lo, c_hi - c_lo, precision,
+                                  real=complex(amp).imag == 0.0)
     if ev is not None:
         ev[1].record()
     t0 = tick("qft", t0)

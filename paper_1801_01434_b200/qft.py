@@ -102,7 +102,7 @@ def build_twiddles(q: int, max_width: int = 24) -> TwiddleTable:
 # ------------------------------------------------------------- device engine
 
 def _support_of(state, q: int):
-    """(amps, length, a0, stride, host_input) for any state form.
+    """(amps, length, a0, stride, host_input, real) for any state form.
 
     amps is a device tensor, or a Python complex when every progression slot
     holds the same amplitude (the uniform-comb kernel is selected from the data).
@@ -112,12 +112,13 @@ def _support_of(state, q: int):
         if state.q != q:
             raise ValueError(f"state length {(state.q,)} does not match q={q}")
         if state.full_comb:
-            return state.amp, state.length, state.a0, state.stride, False
-        return state.progression_amplitudes(), state.length, state.a0, state.stride, False
+            return state.amp, state.length, state.a0, state.stride, False, True
+        return (state.progression_amplitudes(), state.length, state.a0, state.stride, False,
+                complex(state.amp).imag == 0.0)
     if isinstance(state, dev.UniformAmplitudes):
         if state.q != q:
             raise ValueError(f"state length {(state.q,)} does not match q={q}")
-        return complex(state.value), q, 0, 1, False
+        return complex(state.value), q, 0, 1, False, True
     if isinstance(state, dev.DeviceSpectrum):
         if state.q != q:
             raise ValueError(f"state length {(state.q,)} does not match q={q}")
@@ -131,20 +132,20 @@ def _support_of(state, q: int):
         host = True
     a0, stride, length = dev.state_progression(data)
     amps = dev.gather_progression(data, a0, stride, length) if length else None
-    uni = dev.progression_uniform(amps, length) if length else None
+    uni, real = dev.progression_kind(amps, length) if length else (None, True)
     if uni is not None:
-        return uni, length, a0, stride, host
-    return amps, length, a0, stride, host
+        return uni, length, a0, stride, host, True
+    return amps, length, a0, stride, host, real
 
 
 def _run(state, q: int, tiles: int, precision: str):
-    amps, length, a0, stride, host = _support_of(state, q)
+    amps, length, a0, stride, host, real = _support_of(state, q)
     if isinstance(amps, complex):
         out, prob, bsum = dev.dft_uniform(amps, length, a0, stride, q, 0, q, tiles=tiles,
                                           scale=1.0 / math.sqrt(q), precision=precision)
     else:
         out, prob, bsum = dev.dft(amps, length, a0, stride, q, 0, q, tiles=tiles,
-                                  scale=1.0 / math.sqrt(q), precision=precision)
+                                  scale=1.0 / math.sqrt(q), precision=precision, real=real)
     spec = dev.DeviceSpectrum(q, out, prob, bsum, precision=precision)
     return spec.numpy() if host else spec
 

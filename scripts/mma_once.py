@@ -1,4 +1,4 @@
-"""One launch each of the DMMA-engine DFT (generic, uniform) at q=2^24: ncu target."""
+"""One launch each of the DMMA-engine DFT (generic complex, generic real, uniform) at q=2^24: ncu target."""
 import math
 import os
 import sys
@@ -16,6 +16,9 @@ q, c0, r, M = 1 << 24, 29, 116, 144631
 a = np.random.default_rng(0).standard_normal(2 * M)
 amps = torch.from_numpy(a).cuda()
 dev.dft(amps, M, c0, r, q, 0, q)
+ra = amps.clone().view(-1, 2)
+ra[:, 1] = 0
+dev.dft(ra.view(-1), M, c0, r, q, 0, q, real=True)
 dev.dft_uniform(complex(1 / math.sqrt(M)), M, c0, r, q, 0, q)
 torch.cuda.synchronize()
 print("ok")

@@ -56,7 +56,7 @@ class OracleOps:
         p = oracle.probabilities(V)
         return torch.from_numpy(V.view(np.float64).copy()), torch.from_numpy(p), torch.tensor([p.sum()])
 
-    def dft(self, amps, length, a0, stride, q, c_begin, c_count, precision):
+    def dft(self, amps, length, a0, stride, q, c_begin, c_count, precision, real=False):
         return self._rows(amps.numpy().view(np.complex128), length, a0, stride, q, c_begin, c_count)
 
     def dft_uniform(self, amp, length, a0, stride, q, c_begin, c_count, precision):

@@ -571,12 +571,15 @@ def test_c_abi_demo_program(tmp_path):
     assert "row64 = 8" in r.stdout
 
 
-@pytest.mark.parametrize("engine", ["vector", "mma"])
-def test_both_fp64_engines_vs_oracle(engine, monkeypatch):
+@pytest.mark.parametrize("engine,real_form", [("vector", "1"), ("mma", "0"), ("mma", "1")])
+def test_both_fp64_engines_vs_oracle(engine, real_form, monkeypatch):
     """The FP64 DFT has two kernels for tiles == 1: the vector Horner kernel and
-    the DMMA (FP64 tensor-core) GEMM-factored kernel.  Both against the oracle on
-    ragged sizes, output shards and the uniform / generic amplitude paths."""
+    the DMMA (FP64 tensor-core) GEMM-factored kernel, the latter in a complex-A
+    and a real-A form (2 DMMAs per k-step; uniform combs and real amplitudes).
+    All against the oracle on ragged sizes, output shards and the uniform /
+    generic / real amplitude paths."""
     monkeypatch.setenv("SHB_DFT_ENGINE", engine)
+    monkeypatch.setenv("SHB_MMA_REAL", real_form)
     rng = np.random.default_rng(21)
     for q, c0, r, M in [(1 << 10, 5, 3, 1), (1 << 10, 5, 3, 255), (1 << 12, 1, 7, 585), (1 << 16, 11, 12, 5461)]:
         supp = c0 + r * np.arange(M, dtype=np.uint64)
@@ -591,6 +594,31 @@ def test_both_fp64_engines_vs_oracle(engine, monkeypatch):
             ou, pu, bu = dev.dft_uniform(0.3 - 0.1j, M, c0, r, q, lo, cnt)
             refu = oracle.dft_rows(supp, np.full(M, 0.3 - 0.1j), q, rows)
             assert np.max(np.abs(ou.cpu().numpy().view(np.complex128) - refu)) < 1e-12 * max(1, np.abs(refu).max())
+            re_h = rng.standard_normal(M) + 0j
+            re_d = torch.from_numpy(re_h.view(np.float64)).cuda()
+            orl, prl, brl = dev.dft(re_d, M, c0, r, q, lo, cnt, real=True)
+            refr = oracle.dft_rows(supp, re_h, q, rows)
+            assert np.max(np.abs(orl.cpu().numpy().view(np.complex128) - refr)) < 1e-12 * max(1, np.abs(refr).max())
+            assert abs(dev.dsum(brl) - float(prl.sum())) <= 1e-9 * float(prl.sum())
+
+
+def test_dense_dft_selects_real_form_for_real_states():
+    """qft.dense_dft on a real non-uniform state takes shb_dft_real (the data
+    decides, as it does for the uniform comb) and matches the oracle."""
+    rng = np.random.default_rng(5)
+    q = 1 << 14
+    st = np.zeros(q, complex)
+    supp = np.arange(3, q, 9, dtype=np.uint64)
+    st[supp.astype(np.int64)] = rng.standard_normal(supp.size)
+    st /= np.linalg.norm(st)
+    amps, length, a0, stride, host, real = qft._support_of(st, q)
+    assert real and not isinstance(amps, complex) and (a0, stride, length) == (3, 9, supp.size)
+    out = np.asarray(qft.dense_dft(st, qft.build_twiddles(q), qft.KernelPlan()))
+    rows = np.arange(q, dtype=np.uint64)
+    ref = oracle.dft_rows(supp, st[supp.astype(np.int64)], q, rows)
+    assert np.max(np.abs(out - ref)) < 1e-12
+    st[5] = 1e-3j  # one complex amplitude: the complex form
+    assert not qft._support_of(st, q)[5]
 
 
 # ------------------------------------------------------------ SPEC acceptance
