@@ -33,6 +33,7 @@
 //
 // The epilogue fuses |V|^2 (hypot^2, as np.abs(.)**2, qstate.py:111) and a
 // deterministic per-CTA sum of it (norm check, qstate.py:50-53).
+#include <cuda_bf16.h>
 #include <math.h>
 #include <stdlib.h>
 #include <vector>
@@ -688,6 +689,207 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, S
     }
 }
 
+// ---------------------------------------------------------------------------
+// FP32 fast path on the BF16 tensor cores (precision = SHB_FP32, uniform comb,
+// tiles == 1).  Same GEMM factorisation as the DMMA engine with 16-row blocks:
+// j = (jb*16 + j1)*TC_BK + k,
+//   T_jb[j1, c] = sum_k 1 * G[k, c],  G[k, c] = e^{+2 pi i k stride c / q}
+// as mma.sync m16n8k16 bf16 -> f32 with A = 1 (the uniform amplitude is
+// factored out of the sum, exact in bf16) and G split into two bf16 terms,
+// G = G_hi + G_lo (|G - G_hi - G_lo| <= 2^-18 |G|): 4 MMAs per k-step (Re/Im x
+// hi/lo), FP32 accumulation.  Per lane the blocks are folded by an FP32 Horner
+// (U = w^{-16 TC_BK}); every TC_SEG_BLOCKS blocks the FP32 partial is rotated
+// by the exact-index seed (sincospif of the exact integer phase index) and
+// added to an FP64 total.  Error budget (<= 1e-4 relative on |V|^2, SPEC
+// north star): G split 2^-18, FP32 Horner over <= 16 steps, FP32 seeds
+// ~2e-7 -- measured max|dp|/max p in tests/bench.
+#ifndef SHB_TC_BK
+#define SHB_TC_BK 64
+#endif
+#ifndef SHB_TC_SEG
+#define SHB_TC_SEG 32768
+#endif
+constexpr int TC_BK = SHB_TC_BK;          // k extent per block row
+constexpr int TC_KS = TC_BK / 16;         // k-steps of 16
+constexpr int TC_BLOCK = 16 * TC_BK;      // amplitudes per block
+constexpr int TC_SEG_BLOCKS = SHB_TC_SEG / TC_BLOCK > 0 ? SHB_TC_SEG / TC_BLOCK : 1;
+constexpr int TC_WARPS = 8;
+constexpr int TC_OUT_PER_CTA = TC_WARPS * 8;  // 64
+
+__device__ __forceinline__ void hmma_bf16_16816(float (&d)[4], uint32_t a, uint32_t b0, uint32_t b1)
+{
+    // A = all ones (every A register holds the same bf16x2 pair)
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%4,%4,%4}, {%5,%6}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a), "r"(b0), "r"(b1));
+}
+
+// e^{+2 pi i idx / q} in FP32 from the exact integer index (folded to (-q/2, q/2])
+__device__ __forceinline__ void phase_f32(uint64_t idx, uint64_t q, double two_over_q, float &c, float &s)
+{
+    const int64_t sidx = (idx > (q >> 1)) ? (int64_t)(idx - q) : (int64_t)idx;
+    sincospif((float)((double)sidx * two_over_q), &s, &c);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo_elem, float hi_elem)
+{
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo_elem, hi_elem);  // .x -> low 16 bits
+    return *reinterpret_cast<const uint32_t *>(&v);
+}
+
+#ifndef SHB_TC_MINB
+#define SHB_TC_MINB 2
+#endif
+__global__ void __launch_bounds__(TC_WARPS * 32, SHB_TC_MINB) dft_tc32_uniform_kernel(const MmaArgs p)
+{
+    __shared__ double red_tmp[TC_WARPS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t q = p.q, qmask = q - 1;
+    const uint64_t nblocks = (p.length + TC_BLOCK - 1) / TC_BLOCK;
+    const uint64_t tile = (uint64_t)blockIdx.x * TC_OUT_PER_CTA + (uint64_t)warp * 8;
+    const int g = lane >> 2, t4 = lane & 3;
+    // B fragment (16 x 8, col): lane holds k = 2 t4 + {0,1} and 2 t4 + 8 + {0,1}, column n = g
+    const uint64_t cB = p.c_begin + tile + g;
+    uint32_t brh[TC_KS][2], brl[TC_KS][2], bih[TC_KS][2], bil[TC_KS][2];
+#pragma unroll
+    for (int ks = 0; ks < TC_KS; ks++)
+#pragma unroll
+        for (int hlf = 0; hlf < 2; hlf++) {
+            float gr[2], gi[2], grl[2], gil[2];
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const uint64_t k = (uint64_t)ks * 16 + hlf * 8 + 2 * t4 + e;
+                phase_f32((k * p.stride * cB) & qmask, q, p.two_over_q, gr[e], gi[e]);
+                grl[e] = gr[e] - __bfloat162float(__float2bfloat16_rn(gr[e]));
+                gil[e] = gi[e] - __bfloat162float(__float2bfloat16_rn(gi[e]));
+            }
+            brh[ks][hlf] = pack_bf16x2(gr[0], gr[1]);
+            bih[ks][hlf] = pack_bf16x2(gi[0], gi[1]);
+            brl[ks][hlf] = pack_bf16x2(grl[0], grl[1]);
+            bil[ks][hlf] = pack_bf16x2(gil[0], gil[1]);
+        }
+    // D fragment (16 x 8): rows g, g+8; columns 2 t4 + {0,1}.  Per (row, col):
+    // FP32 Horner h over blocks, FP64 total v.
+    uint64_t cD[2];
+    float ur[2], ui[2];
+    float hr[2][2], hi[2][2];  // [row half][col]
+    double vr[2], vi[2];       // [col] (rows merged after seeding)
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+        cD[e] = p.c_begin + tile + 2 * t4 + e;
+        float co, si;
+        phase_f32(((uint64_t)TC_BLOCK * p.stride * cD[e]) & qmask, q, p.two_over_q, co, si);
+        ur[e] = co;
+        ui[e] = -si;  // w^{-TC_BLOCK}
+        vr[e] = vi[e] = 0.0;
+        hr[0][e] = hr[1][e] = hi[0][e] = hi[1][e] = 0.f;
+    }
+    const uint32_t ones = 0x3F803F80u;  // bf16x2 (1, 1)
+    for (uint64_t jb = 0; jb < nblocks; jb++) {
+        float dr[4] = {0.f, 0.f, 0.f, 0.f}, di[4] = {0.f, 0.f, 0.f, 0.f};
+        float drl[4] = {0.f, 0.f, 0.f, 0.f}, dil[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint64_t jblk = jb * TC_BLOCK;
+        if (jblk + TC_BLOCK <= p.length) {
+#pragma unroll
+            for (int ks = 0; ks < TC_KS; ks++) {
+                hmma_bf16_16816(dr, ones, brh[ks][0], brh[ks][1]);
+                hmma_bf16_16816(di, ones, bih[ks][0], bih[ks][1]);
+                hmma_bf16_16816(drl, ones, brl[ks][0], brl[ks][1]);
+                hmma_bf16_16816(dil, ones, bil[ks][0], bil[ks][1]);
+            }
+        } else {
+            // ragged last block: rows j1 whose k range leaves the progression
+            // take A = 0 (per row half) -- A rows are g (a0, a2 regs) and g+8
+            // (a1, a3); a k-step column range is 16 wide, so mask per element
+#pragma unroll
+            for (int ks = 0; ks < TC_KS; ks++) {
+                // A fragment elements: row g / g+8, k = ks*16 + 2 t4 + {0,1} (+8)
+                uint32_t a[4];
+#pragma unroll
+                for (int rr = 0; rr < 2; rr++)
+#pragma unroll
+                    for (int hlf = 0; hlf < 2; hlf++) {
+                        const uint64_t row = (uint64_t)g + 8 * rr;
+                        const uint64_t j0 = jblk + row * TC_BK + (uint64_t)ks * 16 + hlf * 8 + 2 * t4;
+                        const float e0 = j0 < p.length ? 1.f : 0.f, e1 = j0 + 1 < p.length ? 1.f : 0.f;
+                        a[hlf * 2 + rr] = pack_bf16x2(e0, e1);
+                    }
+                auto mma4 = [&](float (&d)[4], uint32_t b0, uint32_t b1) {
+                    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, "
+                                 "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+                };
+                mma4(dr, brh[ks][0], brh[ks][1]);
+                mma4(di, bih[ks][0], bih[ks][1]);
+                mma4(drl, brl[ks][0], brl[ks][1]);
+                mma4(dil, bil[ks][0], bil[ks][1]);
+            }
+        }
+        // FP32 Horner over blocks: h = h * U + T   (T = hi + lo products)
+#pragma unroll
+        for (int rr = 0; rr < 2; rr++)
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const float tr_ = dr[rr * 2 + e] + drl[rr * 2 + e];
+                const float ti_ = di[rr * 2 + e] + dil[rr * 2 + e];
+                const float nr = fmaf(hr[rr][e], ur[e], fmaf(-hi[rr][e], ui[e], tr_));
+                const float ni = fmaf(hr[rr][e], ui[e], fmaf(hi[rr][e], ur[e], ti_));
+                hr[rr][e] = nr;
+                hi[rr][e] = ni;
+            }
+        if ((jb + 1) % TC_SEG_BLOCKS == 0 || jb + 1 == nblocks) {
+            // seed of row j1's last block: a0 + (TC_BLOCK jb + TC_BK j1) * stride
+#pragma unroll
+            for (int rr = 0; rr < 2; rr++) {
+                const uint64_t a_row = p.a0 + (jb * TC_BLOCK + (uint64_t)(g + 8 * rr) * TC_BK) * p.stride;
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    float sc, ss;
+                    phase_f32((a_row * cD[e]) & qmask, q, p.two_over_q, sc, ss);
+                    const double xr = hr[rr][e], xi = hi[rr][e];
+                    vr[e] = fma((double)sc, xr, fma(-(double)ss, xi, vr[e]));
+                    vi[e] = fma((double)sc, xi, fma((double)ss, xr, vi[e]));
+                    hr[rr][e] = hi[rr][e] = 0.f;
+                }
+            }
+        }
+    }
+    // sum over the 16 rows: lanes with equal t4 (xor 4, 8, 16); lanes 0..3 write
+    double psum = 0.0;
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            vr[e] += __shfl_xor_sync(0xffffffffu, vr[e], o);
+            vi[e] += __shfl_xor_sync(0xffffffffu, vi[e], o);
+        }
+        const uint64_t ci = cD[e] - p.c_begin;
+        if (g == 0 && ci < p.c_count) {
+            const double o_re = vr[e] * p.out_re - vi[e] * p.out_im;
+            const double o_im = vr[e] * p.out_im + vi[e] * p.out_re;
+            p.out[ci] = make_double2(o_re, o_im);
+            const double hh = hypot(o_re, o_im);
+            const double pr = hh * hh;
+            if (p.prob) p.prob[ci] = pr;
+            psum += pr;
+        }
+    }
+    if (p.block_sums) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) psum += __shfl_down_sync(0xffffffffu, psum, o);
+        if (lane == 0) red_tmp[warp] = psum;
+        __syncthreads();
+        if (tid == 0) {
+            double b = 0.0;
+#pragma unroll
+            for (int w = 0; w < TC_WARPS; w++) b += red_tmp[w];
+            p.block_sums[blockIdx.x] = b;
+        }
+    }
+}
+
 // Fold MMA per-CTA |V|^2 sums (128 outputs each) into the vector-kernel layout
 // the caller allocated (shb_dft_num_blocks: DFT_THREADS*K outputs per slot), in
 // a fixed order so the norm stays deterministic.
@@ -732,6 +934,39 @@ static int launch_dft_mma(MmaArgs a, cudaStream_t st)
     }
     SHB_TRY_CUDA(cudaGetLastError());
     return SHB_OK;
+}
+
+static int launch_dft_tc32_uniform(MmaArgs a, cudaStream_t st)
+{
+    const uint64_t nblk = (a.c_count + TC_OUT_PER_CTA - 1) / TC_OUT_PER_CTA;
+    if (nblk > 0x7FFFFFFFull) return set_error(SHB_EINVAL, "too many outputs for one launch");
+    double *caller_sums = a.block_sums;
+    Scratch part;
+    if (caller_sums) {
+        SHB_TRY(scratch_alloc(part, sizeof(double) * nblk, st));
+        a.block_sums = (double *)part.ptr;
+    }
+    dft_tc32_uniform_kernel<<<(unsigned)nblk, TC_WARPS * 32, 0, st>>>(a);
+    SHB_LAUNCHED();
+    if (caller_sums) {
+        // caller layout: shb_dft_num_blocks(c_count, SHB_FP32) slots of DFT_THREADS*K outputs
+        constexpr int group = DFT_THREADS * Prec<float>::K / TC_OUT_PER_CTA;
+        static_assert(group * TC_OUT_PER_CTA == DFT_THREADS * Prec<float>::K, "slot sizes must nest");
+        const uint64_t nout = (a.c_count + DFT_THREADS * Prec<float>::K - 1) / (DFT_THREADS * Prec<float>::K);
+        group_sums_kernel<<<(unsigned)((nout + 255) / 256), 256, 0, st>>>((const double *)part.ptr, nblk, group,
+                                                                          caller_sums, nout);
+        SHB_LAUNCHED();
+    }
+    SHB_TRY_CUDA(cudaGetLastError());
+    return SHB_OK;
+}
+
+// FP32 fast path for the uniform comb: the BF16 tensor-core form (tiles == 1),
+// SHB_FP32_ENGINE=vector selects the FP32 Horner kernel instead.
+static bool use_tc32_engine()
+{
+    const char *e = getenv("SHB_FP32_ENGINE");
+    return !(e && e[0] == 'v');
 }
 
 // Engine choice for FP64, tiles == 1 (measured, profiles/r01_mma_real.json):
@@ -853,7 +1088,14 @@ extern "C" int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, ui
     a.out_re = amp_re * scale;
     a.out_im = amp_im * scale;
     cudaStream_t st = as_stream(stream);
-    if (precision == SHB_FP32) return launch_dft<float, true>(a, length, tiles, st);
+    if (precision == SHB_FP32) {
+        if (tiles == 1 && length && use_tc32_engine()) {
+            MmaArgs m{nullptr, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
+                      1.0, 0.0, a.out_re, a.out_im, (double2 *)d_out, d_prob, d_block_sums};
+            return launch_dft_tc32_uniform(m, st);
+        }
+        return launch_dft<float, true>(a, length, tiles, st);
+    }
     if (tiles == 1 && length && use_mma_engine(true, q)) {
         // the amplitude is factored out (out factor = amp*scale): the MMA runs on ones
         MmaArgs m{nullptr, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
@@ -870,6 +1112,10 @@ extern "C" int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, ui
 extern "C" const char *shb_dft_engine(int uniform, int real, uint64_t q, int precision, uint32_t tiles,
                                       int *flops_per_term)
 {
+    if (precision == SHB_FP32 && uniform && tiles == 1 && use_tc32_engine()) {
+        if (flops_per_term) *flops_per_term = 8;  // 4 bf16 MACs: (Re, Im) x (hi, lo)
+        return "dft_tc32_uniform_kernel";
+    }
     const bool mma = precision == SHB_FP64 && tiles == 1 && use_mma_engine(uniform != 0, q);
     const bool realf = mma && (uniform || real) && use_real_form();
     if (flops_per_term) *flops_per_term = realf ? 4 : 8;

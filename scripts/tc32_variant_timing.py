@@ -1,0 +1,42 @@
+"""FP32 fast path variants (scripts/build_tc32_variants.sh): time and accuracy
+of the uniform-comb FP32 DFT against the FP64 DMMA spectrum (max|dp|/max p,
+the 1e-4 bar) at q = 2^24 (n=3127 comb) and optionally q = 2^30 (bench comb)."""
+import json
+import math
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+from paper_1801_01434_b200 import _native as nat  # noqa: E402
+from paper_1801_01434_b200 import device as dev  # noqa: E402
+
+cases = [(1 << 24, 29, 116, 144631)]
+if len(sys.argv) > 1 and sys.argv[1] == "big":
+    cases.append((1 << 30, 10943, 16020, 67025))
+libs = sorted(Path(nat.LIB_PATH.parent / "_variants").glob("*.so")) + [nat.LIB_PATH]
+for q, c0, r, M in cases:
+    amp = complex(1 / math.sqrt(M))
+    nat._lib = nat.load(nat.LIB_PATH)
+    _, p64, _ = dev.dft_uniform(amp, M, c0, r, q, 0, q, precision="fp64")
+    pmax = float(p64.max())
+    for so in libs:
+        nat._lib = nat.load(so)
+        fn = lambda: dev.dft_uniform(amp, M, c0, r, q, 0, q, precision="fp32")  # noqa: E731
+        o = fn()
+        del o
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out, p32, bs = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        err = float((p32 - p64).abs().max()) / pmax
+        print(json.dumps({"q": f"2^{q.bit_length() - 1}", "lib": so.name, "ms": round(ms, 2),
+                          "Gterms/s": round(q * M / ms / 1e6, 1), "max_dp_over_max_p": err,
+                          "norm": dev.dsum(bs)}), flush=True)
+        del out, p32, bs
+        torch.cuda.empty_cache()

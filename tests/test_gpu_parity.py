@@ -196,6 +196,34 @@ def test_fp32_fast_path(golden_dir):
     assert np.max(np.abs(pu32 - p64)) / p64.max() <= 1e-4
 
 
+@pytest.mark.parametrize("engine", ["vector", "tc"])
+def test_fp32_engines_uniform_vs_oracle(engine, monkeypatch):
+    """The FP32 fast path for a uniform comb: the FP32 Horner kernel and the
+    BF16 tensor-core form (G = G_hi + G_lo, FP32 accumulation, FP64 segment
+    sums).  Against the oracle rows at the stated tolerance, max|dp|/max p
+    <= 1e-4 (and |dV| <= 1e-4 max|V|), on ragged lengths (partial last
+    block, M < one block), output shards and a q = 2^24 comb."""
+    monkeypatch.setenv("SHB_FP32_ENGINE", engine)
+    amp = 0.3 - 0.1j
+    for q, c0, r, M in [(1 << 10, 5, 3, 1), (1 << 10, 5, 3, 255), (1 << 12, 1, 7, 585), (1 << 16, 11, 12, 5461),
+                        (1 << 20, 3, 1, (1 << 20) - 3), (1 << 24, 29, 116, 144631)]:
+        rows = np.unique(np.concatenate([np.arange(0, min(q, 4096)), np.arange(q - 130, q),
+                                         np.random.default_rng(q).integers(0, q, 2000)])).astype(np.uint64)
+        supp = c0 + r * np.arange(M, dtype=np.uint64)
+        ref = oracle.dft_rows(supp, np.full(M, amp), q, rows)
+        pref = np.abs(ref) ** 2
+        for lo, cnt in [(0, q), (77, min(q - 77, 129)), (q - 130, 130)]:
+            out, prob, bs = dev.dft_uniform(amp, M, c0, r, q, lo, cnt, precision="fp32")
+            sel = (rows >= lo) & (rows < lo + cnt)
+            o = out.cpu().numpy().view(np.complex128)[(rows[sel] - lo).astype(np.int64)]
+            pm = M * abs(amp) / math.sqrt(q)  # |V_0|, the peak of a uniform comb
+            assert np.max(np.abs(o - ref[sel])) <= 1e-4 * pm, (q, M, lo)
+            pr = prob.cpu().numpy()[(rows[sel] - lo).astype(np.int64)]
+            assert np.max(np.abs(pr - pref[sel])) <= 1e-4 * pm ** 2, (q, M, lo)
+            assert abs(dev.dsum(bs) - float(prob.sum())) <= 1e-6 * float(prob.sum())
+            del out, prob, bs
+
+
 def test_random_states_dense_tiled(golden_dir):
     d = np.load(golden_dir / "random_states.npz")
     for key in ("16", "256", "1024", "4096", "sparse2048"):
