@@ -367,10 +367,22 @@ def run_b200(args):
         if world > 1:
             torch.distributed.all_reduce(err, op=torch.distributed.ReduceOp.MAX)
             torch.distributed.all_reduce(t32, op=torch.distributed.ReduceOp.MAX)
+        f32 = ctypes_int()
+        k32 = lib.shb_dft_engine(1, 1, q, nat.FP32, 1, f32)
+        k32 = k32.decode() if k32 else "dft"
+        tf32 = f32.value * q * M / (float(t32.item()) / 1000.0) / 1e12
         line["fp32_fast_path"] = {
             "dft_ms": float(t32.item()), "phase_terms_per_s": q * M / (float(t32.item()) / 1000.0),
             "max_abs_dp_over_max_p": float(err[0] / err[1]), "tolerance": 1e-4,
-            "m": rec32.m, "m_equal_fp64": rec32.m == rec.m, "note": "DFT kernel only; not the headline (FP64)"}
+            "m": rec32.m, "m_equal_fp64": rec32.m == rec.m, "kernel": f"shb::{k32}",
+            "achieved_tflops": tf32, "flops_per_phase_term": f32.value,
+            "note": "DFT kernel only; not the headline (FP64).  The tensor-core form issues 4 bf16 MACs per "
+                    "phase term (Re/Im x hi/lo split of the phase matrix) on mma.sync m16n8k16; "
+                    "scripts/lowp_mma_probe.cu measures 540 TFLOP/s for that instruction on this GPU"}
+        peaks = _measured_peaks()
+        if peaks.get("bf16_tflops") and "tc32" in k32:
+            line["fp32_fast_path"]["frac_of_bf16_peak"] = tf32 / peaks["bf16_tflops"]
+            line["fp32_fast_path"]["bf16_peak_source"] = "MEASURED_PEAKS.json bf16_tflops (cuBLAS, tcgen05)"
 
     if not args.no_factoring:
         from paper_1801_01434_b200 import qft
@@ -400,6 +412,13 @@ def run_b200(args):
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def _measured_peaks() -> dict:
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        return {}
 
 
 def ctypes_int():

@@ -408,6 +408,9 @@ constexpr int MMA_OUT_PER_CTA = MMA_WARPS * MMA_CT * 8;  // 64
 #ifndef SHB_MMA_GREC
 #define SHB_MMA_GREC 1  // G fragments by recurrence from 2 exact phases
 #endif
+#ifndef SHB_MMA_STAGGER
+#define SHB_MMA_STAGGER 0  // ns the upper 4 warps wait before their first block
+#endif
 #ifndef SHB_MMA_SEG
 #define SHB_MMA_SEG 32768  // amplitudes between exact per-lane re-seeds
 #endif
@@ -537,6 +540,11 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, S
     }
 
     const double amp_r = p.amp_re, amp_i = p.amp_im;
+#if SHB_MMA_STAGGER > 0
+    // the two warps sharing an SMSP (w, w + 4) would otherwise drain their
+    // DMMA chains at the same time at every block boundary
+    if (warp >= 4 && warp < 8) __nanosleep(SHB_MMA_STAGGER);
+#endif
     // Software pipeline over blocks (NP = 2 accumulator sets): iteration jb
     // issues block jb's DMMAs into set jb&1, then folds block jb-1 from the
     // other set, so the fold (which waits on the last DMMA of its block) sits

@@ -106,3 +106,34 @@ def test_c_abi_demo_compiles_and_links(lib, tmp_path):
     # plain C against include/shorb200.h and the .so (running it needs a GPU: test_gpu_parity)
     from conftest import build_c_demo
     assert build_c_demo(tmp_path).exists()
+
+
+def test_dft_engine_choice(lib, monkeypatch):
+    """shb_dft_engine names the kernel each DFT entry point launches (no GPU
+    call): real-A DMMA for uniform combs and real amplitudes (4 flops per
+    phase term), complex DMMA otherwise (8), the vector kernel for tiles > 1,
+    the BF16 tensor-core form for the FP32 uniform comb; env overrides."""
+    import ctypes
+
+    def eng(uniform, real, q=1 << 30, prec=nat.FP64, tiles=1):
+        f = ctypes.c_int(0)
+        name = lib.shb_dft_engine(uniform, real, q, prec, tiles, ctypes.byref(f)).decode()
+        return name, f.value
+
+    for var in ("SHB_DFT_ENGINE", "SHB_MMA_REAL", "SHB_FP32_ENGINE"):
+        monkeypatch.delenv(var, raising=False)
+    assert eng(1, 1) == ("dft_mma_kernel<uniform, real A>", 4)
+    assert eng(0, 1) == ("dft_mma_kernel<generic, real A>", 4)
+    assert eng(0, 0) == ("dft_mma_kernel<generic, complex A>", 8)
+    assert eng(1, 1, tiles=4)[0] == "dft_kernel<uniform>"
+    assert eng(1, 1, prec=nat.FP32) == ("dft_tc32_uniform_kernel", 8)
+    assert eng(0, 1, prec=nat.FP32)[0] == "dft_kernel<generic>"
+    # the choice never depends on the output range, only on q and the data
+    assert eng(1, 1, q=1 << 8) == eng(1, 1, q=1 << 32)
+    monkeypatch.setenv("SHB_DFT_ENGINE", "vector")
+    assert eng(1, 1) == ("dft_kernel<uniform>", 8)
+    monkeypatch.setenv("SHB_DFT_ENGINE", "mma")
+    monkeypatch.setenv("SHB_MMA_REAL", "0")
+    assert eng(1, 1) == ("dft_mma_kernel<uniform, complex A>", 8)
+    monkeypatch.setenv("SHB_FP32_ENGINE", "vector")
+    assert eng(1, 1, prec=nat.FP32)[0] == "dft_kernel<uniform>"
