@@ -977,7 +977,7 @@ static bool use_tc32_engine()
     return !(e && e[0] == 'v');
 }
 
-// Engine choice for FP64, tiles == 1 (measured, profiles/r01_mma_real.json):
+// Engine choice for FP64, tiles == 1 (measured, profiles/r01_mma_real.jsonl):
 // * uniform comb and real amplitudes: the real-A DMMA form, 2 real products
 //   per phase term (7.7-8.0e12 terms/s at q = 2^24 and 2^30, vs 4.3e12 for the
 //   vector Horner kernel, whose complex recurrence needs 4 FP64 ops per term
