@@ -397,7 +397,10 @@ static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t s
 #define SHB_MMA_MINB 1
 #endif
 constexpr int MMA_CT = SHB_MMA_CT;         // 8-output tiles per warp
-constexpr int MMA_WARPS = 8;               // consumer warps
+#ifndef SHB_MMA_WARPS
+#define SHB_MMA_WARPS 8
+#endif
+constexpr int MMA_WARPS = SHB_MMA_WARPS;   // consumer warps
 constexpr int MMA_OUT_PER_CTA = MMA_WARPS * MMA_CT * 8;  // 64
 #ifndef SHB_MMA_NACC
 #define SHB_MMA_NACC 1  // accumulator sets by k-step parity (real form)
@@ -407,9 +410,6 @@ constexpr int MMA_OUT_PER_CTA = MMA_WARPS * MMA_CT * 8;  // 64
 #endif
 #ifndef SHB_MMA_GREC
 #define SHB_MMA_GREC 1  // G fragments by recurrence from 2 exact phases
-#endif
-#ifndef SHB_MMA_STAGGER
-#define SHB_MMA_STAGGER 0  // ns the upper 4 warps wait before their first block
 #endif
 #ifndef SHB_MMA_SEG
 #define SHB_MMA_SEG 32768  // amplitudes between exact per-lane re-seeds
@@ -540,11 +540,6 @@ __global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, S
     }
 
     const double amp_r = p.amp_re, amp_i = p.amp_im;
-#if SHB_MMA_STAGGER > 0
-    // the two warps sharing an SMSP (w, w + 4) would otherwise drain their
-    // DMMA chains at the same time at every block boundary
-    if (warp >= 4 && warp < 8) __nanosleep(SHB_MMA_STAGGER);
-#endif
     // Software pipeline over blocks (NP = 2 accumulator sets): iteration jb
     // issues block jb's DMMAs into set jb&1, then folds block jb-1 from the
     // other set, so the fold (which waits on the last DMMA of its block) sits
