@@ -393,15 +393,30 @@ static int launch_dft(DftArgs a, uint64_t length, uint32_t tiles, cudaStream_t s
 #ifndef SHB_MMA_CT
 #define SHB_MMA_CT 1
 #endif
-#ifndef SHB_MMA_MINB
-#define SHB_MMA_MINB 1
+constexpr int MMA_CT = SHB_MMA_CT;  // 8-output tiles per warp
+// CTA shapes (measured, scripts/build_mma_real_variants.sh): the uniform path
+// (254 registers) runs one CTA of 8 warps per SM; the amplitude-stream path
+// (168-register cap with its producer warp) runs two CTAs of 4 consumer warps
+// (+7 % on real amplitudes against one CTA of 8).
+#ifndef SHB_MMA_WARPS_U
+#define SHB_MMA_WARPS_U 8
 #endif
-constexpr int MMA_CT = SHB_MMA_CT;         // 8-output tiles per warp
-#ifndef SHB_MMA_WARPS
-#define SHB_MMA_WARPS 8
+#ifndef SHB_MMA_WARPS_G
+#define SHB_MMA_WARPS_G 4
 #endif
-constexpr int MMA_WARPS = SHB_MMA_WARPS;   // consumer warps
-constexpr int MMA_OUT_PER_CTA = MMA_WARPS * MMA_CT * 8;  // 64
+#ifndef SHB_MMA_MINB_U
+#define SHB_MMA_MINB_U 1
+#endif
+#ifndef SHB_MMA_MINB_G
+#define SHB_MMA_MINB_G 2
+#endif
+template <bool UNIF>
+struct MmaShape {
+    static constexpr int WARPS = UNIF ? SHB_MMA_WARPS_U : SHB_MMA_WARPS_G;  // consumer warps
+    static constexpr int MINB = UNIF ? SHB_MMA_MINB_U : SHB_MMA_MINB_G;
+    static constexpr int THREADS = UNIF ? WARPS * 32 : WARPS * 32 + 32;    // + TMA producer warp
+    static constexpr int OUT_PER_CTA = WARPS * MMA_CT * 8;
+};
 #ifndef SHB_MMA_NACC
 #define SHB_MMA_NACC 1  // accumulator sets by k-step parity (real form)
 #endif
@@ -447,9 +462,11 @@ struct MmaArgs {
 // DMMA chains alternate between two accumulator sets by k-step parity so that
 // dependent DMMAs on one accumulator are 4 instructions apart.
 template <bool UNIF, bool REALA>
-__global__ void __launch_bounds__(UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32, SHB_MMA_MINB)
+__global__ void __launch_bounds__(MmaShape<UNIF>::THREADS, MmaShape<UNIF>::MINB)
     dft_mma_kernel(const MmaArgs p)
 {
+    constexpr int MMA_WARPS = MmaShape<UNIF>::WARPS;
+    constexpr int MMA_OUT_PER_CTA = MmaShape<UNIF>::OUT_PER_CTA;
     constexpr int MMA_B = UNIF ? SHB_MMA_BU : SHB_MMA_B;  // k extent per block row
     constexpr int MMA_KS = MMA_B / 4;                      // k-steps of 4
     constexpr int MMA_BLOCK = 8 * MMA_B;                   // amplitudes per block
@@ -916,9 +933,10 @@ static int launch_dft_mma(MmaArgs a, cudaStream_t st)
     if (smem)
         SHB_TRY_CUDA(cudaFuncSetAttribute(dft_mma_kernel<UNIF, REALA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
+    constexpr int MMA_OUT_PER_CTA = MmaShape<UNIF>::OUT_PER_CTA;
     const uint64_t nblk = (a.c_count + MMA_OUT_PER_CTA - 1) / MMA_OUT_PER_CTA;
     if (nblk > 0x7FFFFFFFull) return set_error(SHB_EINVAL, "too many outputs for one launch");
-    const unsigned nthreads = UNIF ? MMA_WARPS * 32 : MMA_WARPS * 32 + 32;
+    const unsigned nthreads = MmaShape<UNIF>::THREADS;
     double *caller_sums = a.block_sums;
     Scratch part;
     if (caller_sums) {
