@@ -296,8 +296,9 @@ def run_b200(args):
     # FP64 rate (SMs x 64 DFMA/clk x 2 flops) at the SM clock measured during
     # the timed region -- a hard upper bound (MEASURED_PEAKS.json has no FP64
     # figure); the DFMA-chain probe is reported beside it.
-    ptf = ctypes_double()
+    ptf, pdm = ctypes_double(), ctypes_double()
     nat.check(lib.shb_fp64_peak(2.0, ptf, None), "fp64 peak")
+    nat.check(lib.shb_fp64_dmma_peak(2.0, pdm, None), "fp64 dmma peak")
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     clk_mhz = clk.get("sm_mhz") or 1965.0
     peak_tf = sms * 64 * 2 * clk_mhz * 1e6 / 1e12
@@ -330,6 +331,9 @@ def run_b200(args):
                            "(median SM clock in the timed region); MEASURED_PEAKS.json has no FP64 figure",
             "peak_probe": ptf.value,
             "peak_probe_note": "shb_fp64_peak: independent DFMA chains with constant operands on this GPU",
+            "peak_probe_dmma": pdm.value,
+            "peak_probe_dmma_note": "shb_fp64_dmma_peak: independent DMMA m8n8k4 chains on this GPU (the "
+                                    "tensor path of the same FP64 datapath)",
             "kernel": f"shb::{kname}", "dft_ms_per_launch": dft_s * 1000.0,
             "flops_per_phase_term": fpt.value, "flops_per_launch": fpt.value * rec.phase_terms}
 

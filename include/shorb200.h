@@ -45,6 +45,9 @@ uint64_t shb_kernel_launches(void);
  * `seconds` of independent DFMA chains: the roofline denominator of the QFT
  * kernel (MEASURED_PEAKS.json carries HBM and bf16 peaks only). */
 int shb_fp64_peak(double seconds, double *tflops, void *stream);
+/* The same for the FP64 tensor path (DMMA m8n8k4, the QFT's default FP64
+ * engine): independent accumulator chains, about `seconds` long. */
+int shb_fp64_dmma_peak(double seconds, double *tflops, void *stream);
 
 /* ------------------------------------------------------------------ modexp
  * qstate.entangle_modexp (qstate.py:64-83): part 2 of the register.

@@ -30,6 +30,7 @@ SIGNATURES = {
     "shb_device_info": ([_i32, ctypes.POINTER(ctypes.c_int), ctypes.c_char_p, _i32], _i32),
     "shb_kernel_launches": ([], _u64),
     "shb_fp64_peak": ([_f64, _PF64, _vp], _i32),
+    "shb_fp64_dmma_peak": ([_f64, _PF64, _vp], _i32),
     "shb_modexp": ([_vp, _u64, _u64, _u64, _u64, _vp], _i32),
     "shb_class_counts": ([_vp, _u64, _vp, _u64, _vp], _i32),
     "shb_compact_eq": ([_vp, _u64, _u32, _u64, _vp, _u64, _P64, _vp], _i32),

@@ -203,6 +203,30 @@ __global__ void __launch_bounds__(256) fp64_probe_kernel(double *out, int iters,
     if (s == 1234.5) out[0] = s;  // keep the chains alive
 }
 
+// FP64 tensor path (DMMA m8n8k4) probe: 4 independent accumulator chains per
+// warp, B operands cycling through registers, as in the DFT's DMMA kernel.
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double *out, int iters, double a, double b)
+{
+    double d[4][2], g[8];
+#pragma unroll
+    for (int i = 0; i < 4; i++) d[i][0] = d[i][1] = threadIdx.x * 1e-6 + i;
+#pragma unroll
+    for (int i = 0; i < 8; i++) g[i] = b + i * 1e-3;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                             : "+d"(d[i][0]), "+d"(d[i][1])
+                             : "d"(a), "d"(g[k]));
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) s += d[i][0] + d[i][1];
+    if (s == 1234.5) out[0] = s;
+}
+
 }  // namespace shb
 
 using namespace shb;
@@ -258,6 +282,41 @@ int shb_fp64_peak(double seconds, double *tflops, void *stream)
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     const double flops = 2.0 * 16.0 * (double)iters * 256.0 * grid * reps;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    return SHB_OK;
+}
+
+int shb_fp64_dmma_peak(double seconds, double *tflops, void *stream)
+{
+    if (!tflops) return set_error(SHB_EINVAL, "null output");
+    cudaStream_t st = as_stream(stream);
+    Scratch sink;
+    SHB_TRY(scratch_alloc(sink, sizeof(double), st));
+    const unsigned grid = (unsigned)sm_count() * 2;
+    const int iters = 1 << 12;
+    cudaEvent_t e0, e1;
+    SHB_TRY_CUDA(cudaEventCreate(&e0));
+    SHB_TRY_CUDA(cudaEventCreate(&e1));
+    dmma_probe_kernel<<<grid, 256, 0, st>>>((double *)sink.ptr, 64, 0.999999, 1e-7);  // warm-up
+    SHB_LAUNCHED();
+    int reps = 1;
+    float ms = 0.f;
+    for (;;) {
+        SHB_TRY_CUDA(cudaEventRecord(e0, st));
+        for (int r = 0; r < reps; r++) {
+            dmma_probe_kernel<<<grid, 256, 0, st>>>((double *)sink.ptr, iters, 0.999999, 1e-7);
+            SHB_LAUNCHED();
+        }
+        SHB_TRY_CUDA(cudaEventRecord(e1, st));
+        SHB_TRY_CUDA(cudaEventSynchronize(e1));
+        SHB_TRY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (ms >= seconds * 1000.0 * 0.5 || reps >= (1 << 16)) break;
+        reps *= 2;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    // one DMMA m8n8k4 = 256 multiply-adds = 512 flops per warp instruction
+    const double flops = 512.0 * 32.0 * (double)iters * (256 / 32) * grid * reps;
     *tflops = flops / (ms * 1e-3) / 1e12;
     return SHB_OK;
 }

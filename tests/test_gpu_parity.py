@@ -709,3 +709,15 @@ def test_spec_acceptance_10_period_recovery_rate():
             else:
                 assert est.kind == "retry"  # failures are retry-classified
     assert (ok, total) == (78, 106)  # the reference's own outcome on the same draws
+
+
+def test_fp64_peak_probes():
+    """The bench's FP64 roofline probes (DFMA chains and DMMA chains) report a
+    throughput near the nominal 148 SM x 64 FMA/clk x 2 flops (37 TF/s at
+    1.965 GHz): a sanity bound on the denominators the bench prints."""
+    import ctypes
+    lib = nat.load()
+    for fn in (lib.shb_fp64_peak, lib.shb_fp64_dmma_peak):
+        tf = ctypes.c_double()
+        nat.check(fn(0.2, ctypes.byref(tf), None), "probe")
+        assert 15.0 < tf.value < 45.0, tf.value
