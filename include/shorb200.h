@@ -178,6 +178,17 @@ int shb_cumsum_total(const double *d_prob, uint64_t count, double *total,
 int shb_cumsum_search(const double *d_prob, uint64_t count, double target,
                       uint64_t *index, void *stream);
 
+/* Continuations from a running value s_in, for a shard of a longer vector
+ * whose earlier elements summed left to right to s_in (the sharded read
+ * chains them rank to rank):
+ *   *s_out  = the running sum after the last element (s_in if count == 0);
+ *   *index  = first i with running sum s_in + p[0] + ... + p[i] > target,
+ *             or count if none. */
+int shb_cumsum_total_from(const double *d_prob, uint64_t count, double s_in,
+                          double *s_out, void *stream);
+int shb_cumsum_search_from(const double *d_prob, uint64_t count, double s_in,
+                           double target, uint64_t *index, void *stream);
+
 /* The whole Born-rule read (qstate.py:112-114) for a draw u:
  * target = u * cumsum[-1], *index = searchsorted(cumsum, target, "right")
  * (un-clamped; the caller clamps to q-1), *total = cumsum[-1] (nullable). */

@@ -201,6 +201,20 @@ def sample_index_numpy(probs: np.ndarray, u: float) -> int:
     return min(m, probs.size - 1)
 
 
+def cumsum_total_from(probs: np.ndarray, s_in: float) -> float:
+    """Running value of np.cumsum (qstate.py:112, a strictly sequential chain of
+    float64 adds) after `probs`, when the chain stood at s_in before them."""
+    return float(np.cumsum(np.concatenate([[float(s_in)], np.asarray(probs, dtype=np.float64)]))[-1])
+
+
+def cumsum_search_from(probs: np.ndarray, s_in: float, target: float) -> int:
+    """searchsorted(cumsum, target, "right") (qstate.py:113) restricted to a
+    shard whose chain starts at s_in: first i with s_in + p[0] + ... + p[i] >
+    target, else len(probs)."""
+    c = np.cumsum(np.concatenate([[float(s_in)], np.asarray(probs, dtype=np.float64)]))[1:]
+    return int(np.searchsorted(c, target, side="right"))
+
+
 # ---------------------------------------------------------------- closed form
 
 def comb_probabilities(q: int, r: int, c0: int, M: int, rows) -> np.ndarray:

@@ -51,6 +51,8 @@ SIGNATURES = {
     "shb_sum": ([_vp, _u64, _PF64, _vp], _i32),
     "shb_cumsum_total": ([_vp, _u64, _PF64, _vp], _i32),
     "shb_cumsum_search": ([_vp, _u64, _f64, _P64, _vp], _i32),
+    "shb_cumsum_total_from": ([_vp, _u64, _f64, _PF64, _vp], _i32),
+    "shb_cumsum_search_from": ([_vp, _u64, _f64, _f64, _P64, _vp], _i32),
     "shb_sample_index": ([_vp, _u64, _f64, _P64, _PF64, _vp], _i32),
     "shb_dense_dft_host": ([_vp, _u64, _u32, _i32, _vp], _i32),
     "shb_partial_row_sums_host": ([_vp, _vp, _vp, _u64, _u64, _u64, _u64, _u64], _i32),

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) tile_sum_kernel(const double *__restrict_
 
 // pass 2: exclusive prefix of the tile sums (one CTA)
 __global__ void __launch_bounds__(SUM_THREADS) tile_prefix_kernel(const double *__restrict__ tsum, uint64_t nt,
-                                                                 double *__restrict__ tstart)
+                                                                 double s_in, double *__restrict__ tstart)
 {
     __shared__ double part[SUM_THREADS];
     const uint64_t per = (nt + SUM_THREADS - 1) / SUM_THREADS;
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(SUM_THREADS) tile_prefix_kernel(const double *
     part[threadIdx.x] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double run = 0.0;
+        double run = s_in;  // approximate tile starts only predict binades (exactness comes from the walk)
         for (int t = 0; t < SUM_THREADS; t++) {
             const double v = part[t];
             part[t] = run;
@@ -542,7 +542,8 @@ extern "C" int shb_sum(const double *d_x, uint64_t count, double *out, void *str
 }
 
 // exact walk over all tiles -> (total, exact running sum at every tile start)
-static int seq_total(const double *d_prob, uint64_t count, double *tile_S, double *total_host, cudaStream_t st)
+static int seq_total(const double *d_prob, uint64_t count, double s_in, double *tile_S, double *total_host,
+                     cudaStream_t st)
 {
     SHB_TRY(seq_prepare());
     const uint64_t nt = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
@@ -553,11 +554,11 @@ static int seq_total(const double *d_prob, uint64_t count, double *tile_S, doubl
     SHB_TRY(scratch_alloc(recs, sizeof(TileRec) * nt, st));
     tile_sum_kernel<<<(unsigned)nt, 256, 0, st>>>(d_prob, count, (double *)tsum.ptr);
     SHB_LAUNCHED();
-    tile_prefix_kernel<<<1, SUM_THREADS, 0, st>>>((const double *)tsum.ptr, nt, (double *)tstart.ptr);
+    tile_prefix_kernel<<<1, SUM_THREADS, 0, st>>>((const double *)tsum.ptr, nt, s_in, (double *)tstart.ptr);
     SHB_LAUNCHED();
     tile_rec_kernel<<<(unsigned)nt, 256, 0, st>>>(d_prob, count, (const double *)tstart.ptr, (TileRec *)recs.ptr);
     SHB_LAUNCHED();
-    seqscan_kernel<<<1, SEQ_THREADS, seq_smem(), st>>>(d_prob, count, 0, nt, 0.0, 0, 0.0,
+    seqscan_kernel<<<1, SEQ_THREADS, seq_smem(), st>>>(d_prob, count, 0, nt, s_in, 0, 0.0,
                                                          (const TileRec *)recs.ptr, tile_S, (double *)tot.ptr,
                                                          nullptr);
     SHB_LAUNCHED();
@@ -576,7 +577,7 @@ extern "C" int shb_cumsum_total(const double *d_prob, uint64_t count, double *to
     const uint64_t nch = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
     Scratch cs;
     SHB_TRY(scratch_alloc(cs, sizeof(double) * nch, st));
-    return seq_total(d_prob, count, (double *)cs.ptr, total, st);
+    return seq_total(d_prob, count, 0.0, (double *)cs.ptr, total, st);
 }
 
 static int search_from_tiles(const double *d_prob, uint64_t count, const double *d_tile_S, double tot,
@@ -617,7 +618,38 @@ extern "C" int shb_cumsum_search(const double *d_prob, uint64_t count, double ta
     Scratch cs;
     SHB_TRY(scratch_alloc(cs, sizeof(double) * nch, st));
     double tot = 0.0;
-    SHB_TRY(seq_total(d_prob, count, (double *)cs.ptr, &tot, st));
+    SHB_TRY(seq_total(d_prob, count, 0.0, (double *)cs.ptr, &tot, st));
+    return search_from_tiles(d_prob, count, (const double *)cs.ptr, tot, target, index, st);
+}
+
+// Continuations of the sequential cumsum from a running value s_in (a shard of
+// a longer vector whose earlier elements summed, left to right, to s_in): the
+// sharded Born-rule read chains these rank to rank (distributed.py).
+extern "C" int shb_cumsum_total_from(const double *d_prob, uint64_t count, double s_in, double *s_out,
+                                     void *stream)
+{
+    if (!s_out) return set_error(SHB_EINVAL, "null output");
+    *s_out = s_in;
+    if (count == 0) return SHB_OK;
+    cudaStream_t st = as_stream(stream);
+    const uint64_t nch = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    Scratch cs;
+    SHB_TRY(scratch_alloc(cs, sizeof(double) * nch, st));
+    return seq_total(d_prob, count, s_in, (double *)cs.ptr, s_out, st);
+}
+
+extern "C" int shb_cumsum_search_from(const double *d_prob, uint64_t count, double s_in, double target,
+                                      uint64_t *index, void *stream)
+{
+    if (!index) return set_error(SHB_EINVAL, "null output");
+    *index = count;
+    if (count == 0) return SHB_OK;
+    cudaStream_t st = as_stream(stream);
+    const uint64_t nch = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    Scratch cs;
+    SHB_TRY(scratch_alloc(cs, sizeof(double) * nch, st));
+    double tot = s_in;
+    SHB_TRY(seq_total(d_prob, count, s_in, (double *)cs.ptr, &tot, st));
     return search_from_tiles(d_prob, count, (const double *)cs.ptr, tot, target, index, st);
 }
 
@@ -633,7 +665,7 @@ extern "C" int shb_sample_index(const double *d_prob, uint64_t count, double u, 
     Scratch cs;
     SHB_TRY(scratch_alloc(cs, sizeof(double) * nch, st));
     double tot = 0.0;
-    SHB_TRY(seq_total(d_prob, count, (double *)cs.ptr, &tot, st));
+    SHB_TRY(seq_total(d_prob, count, 0.0, (double *)cs.ptr, &tot, st));
     if (total) *total = tot;
     const double target = u * tot;  // s.uniform() * cum[-1] (qstate.py:113)
     return search_from_tiles(d_prob, count, (const double *)cs.ptr, tot, target, index, st);

@@ -216,6 +216,22 @@ def cumsum_search(p, target: float) -> int:
     return int(out.value)
 
 
+def cumsum_total_from(p, s_in: float) -> float:
+    """Running sum after p, continuing a sequential cumsum that stood at s_in."""
+    out = ctypes.c_double(0.0)
+    nat.check(nat.load().shb_cumsum_total_from(_vp(p), p.numel(), float(s_in), ctypes.byref(out), _stream()),
+              "cumsum_total_from")
+    return float(out.value)
+
+
+def cumsum_search_from(p, s_in: float, target: float) -> int:
+    """First i with running sum s_in + p[0] + ... + p[i] > target (sequential), else len(p)."""
+    out = ctypes.c_uint64(0)
+    nat.check(nat.load().shb_cumsum_search_from(_vp(p), p.numel(), float(s_in), float(target),
+                                                ctypes.byref(out), _stream()), "cumsum_search_from")
+    return int(out.value)
+
+
 def sample_index(p, u: float) -> tuple[int, float]:
     """searchsorted(cumsum(p), u * cumsum(p)[-1], "right") exactly, and cumsum(p)[-1]."""
     out = ctypes.c_uint64(0)

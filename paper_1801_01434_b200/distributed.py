@@ -74,6 +74,12 @@ class DeviceOps:
     def sample(self, prob, u):
         return self.dev.sample_index(prob, u)[0]
 
+    def cumsum_total_from(self, prob, s_in):
+        return self.dev.cumsum_total_from(prob, s_in)
+
+    def cumsum_search_from(self, prob, s_in, target):
+        return self.dev.cumsum_search_from(prob, s_in, target)
+
     def empty(self, n, dtype):
         return self.torch.empty(n, dtype=dtype, device=self.device)
 
@@ -183,16 +189,12 @@ def sharded_attempt(n: int, x: int, q: int, sampler: qstate.Sampler, *, rank: in
         norm2 = float(nt.item())
     if abs(math.sqrt(norm2) - 1.0) > qstate.norm_tolerance(precision):
         raise ValueError(f"register is not normalized (|amp| = {math.sqrt(norm2)!r})")
-    # (4) probability shards -> rank 0 -> exact sequential CDF -> m to all ranks
+    # (4) exact sequential CDF (qstate.py:112-113) without gathering the
+    # probabilities: the running sum is chained rank to rank, then the one
+    # rank whose shard holds u * total searches it
     u = sampler.uniform()
     if world > 1:
-        full, _ = _all_gather_var(prob.contiguous(), world, group, torch)  # shards in c order
-        mt = torch.zeros(1, dtype=torch.int64, device=prob.device)
-        if rank == 0:
-            mt[0] = ops.sample(full, u)
-        del full
-        dist.broadcast(mt, src=0, group=group)
-        m = int(mt.item())
+        m = _sharded_sample(ops, prob, u, q, c_lo, rank, world, group, torch)
     else:
         m = ops.sample(prob, u)
     m = min(m, q - 1)
@@ -203,6 +205,43 @@ def sharded_attempt(n: int, x: int, q: int, sampler: qstate.Sampler, *, rank: in
     if keep_spectrum:
         rec.spectrum = (out, prob)
     return rec
+
+
+def _sharded_sample(ops, prob, u: float, q: int, c_lo: int, rank: int, world: int, group, torch) -> int:
+    """searchsorted(np.cumsum(p), u * cumsum[-1], "right") over the c-sharded
+    probability vector, bit-identical to the single-device read.
+
+    np.cumsum is a strictly sequential chain of float64 adds, so the running
+    sum entering shard g is exactly the running sum leaving shard g-1: rank g
+    receives it (one float64), continues the chain over its shard
+    (ops.cumsum_total_from) and sends the result on.  An all_gather of the
+    (enter, leave) pairs gives every rank the total and the shard whose
+    leaving sum first exceeds the target; that rank searches its shard from
+    its entering sum and broadcasts m.  Traffic: O(world) doubles instead of
+    the q-element probability vector."""
+    import torch.distributed as dist
+    # the scalars travel on the device under NCCL, on the host under gloo
+    # (gloo point-to-point takes CPU tensors)
+    dev = prob.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    s_in = torch.zeros(1, dtype=torch.float64, device=dev)
+    if rank > 0:
+        dist.recv(s_in, src=rank - 1, group=group)
+    s_out = torch.tensor([ops.cumsum_total_from(prob, float(s_in.item()))], dtype=torch.float64, device=dev)
+    if rank < world - 1:
+        dist.send(s_out, dst=rank + 1, group=group)
+    pairs = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(world)]
+    dist.all_gather(pairs, torch.cat([s_in, s_out]), group=group)
+    bounds = [(float(t[0].item()), float(t[1].item())) for t in pairs]
+    total = bounds[-1][1]
+    target = u * total
+    owner = next((g for g in range(world) if bounds[g][1] > target), None)
+    if owner is None:  # no running sum exceeds the target: searchsorted returns q
+        return q
+    mt = torch.zeros(1, dtype=torch.int64, device=dev)
+    if rank == owner:
+        mt[0] = c_lo + ops.cumsum_search_from(prob, bounds[owner][0], target)
+    dist.broadcast(mt, src=owner, group=group)
+    return int(mt.item())
 
 
 def dump_spectrum_sharded(out, q: int, path, *, rank: int = 0, world: int = 1, group=None,

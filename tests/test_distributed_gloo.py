@@ -68,6 +68,12 @@ class OracleOps:
     def sample(self, prob, u):
         return oracle.sample_index(prob.numpy(), u)
 
+    def cumsum_total_from(self, prob, s_in):
+        return oracle.cumsum_total_from(prob.numpy(), s_in)
+
+    def cumsum_search_from(self, prob, s_in, target):
+        return oracle.cumsum_search_from(prob.numpy(), s_in, target)
+
     def to_host(self, t):
         return t.numpy()
 

@@ -721,3 +721,37 @@ def test_fp64_peak_probes():
         tf = ctypes.c_double()
         nat.check(fn(0.2, ctypes.byref(tf), None), "probe")
         assert 15.0 < tf.value < 45.0, tf.value
+
+
+def test_chained_device_cumsum_matches_whole_vector(golden_dir):
+    """The device halves of the sharded Born-rule read: shb_cumsum_total_from /
+    shb_cumsum_search_from chained over 2..8 shards of a probability vector
+    give the same total (bitwise) and the same m as shb_sample_index on the
+    whole vector, on the reference's draws and on adversarial vectors (tie
+    storms, long zero runs, subnormals)."""
+    d = np.load(golden_dir / "sampling.npz")
+    rng = np.random.default_rng(17)
+    vecs = [(oracle.probabilities(d["state"]), [float(u) for u, _ in d["draws"]])]
+    ties = np.full(1 << 16, 2.0 ** -20)
+    ties[::3] = 2.0 ** -53
+    zeros = rng.random(1 << 18) * (rng.random(1 << 18) < 0.1)
+    sub = np.concatenate([np.full(1000, 5e-324), rng.random(50000)])
+    vecs += [(v, list(rng.random(40))) for v in (ties, zeros, sub)]
+    for p_h, us in vecs:
+        p = torch.from_numpy(np.ascontiguousarray(p_h)).cuda()
+        n = p_h.size
+        for world in (2, 3, 8):
+            cuts = [0] + sorted(rng.choice(np.arange(1, n), world - 1, replace=False).tolist()) + [n]
+            bounds, s = [], 0.0
+            for g in range(world):
+                s_out = dev.cumsum_total_from(p[cuts[g]:cuts[g + 1]], s)
+                bounds.append((s, s_out))
+                s = s_out
+            m_all, tot = dev.sample_index(p, 0.5)
+            assert s == tot == float(np.cumsum(p_h)[-1])
+            for u in us:
+                target = u * s
+                owner = next((g for g in range(world) if bounds[g][1] > target), None)
+                got = n if owner is None else cuts[owner] + dev.cumsum_search_from(
+                    p[cuts[owner]:cuts[owner + 1]], bounds[owner][0], target)
+                assert got == dev.sample_index(p, u)[0]

@@ -128,3 +128,27 @@ def test_closed_form_comb_vs_reference_rows(golden_dir):
         p_cf = oracle.comb_probabilities(q, info["r"], info["c0"], info["M"], d["rows"])
         # the reference dense rows themselves carry ~1e-11 accumulated rounding at 2^24
         assert np.max(np.abs(p_cf - p_ref)) / np.max(p_ref) < 1e-10
+
+
+def test_chained_cumsum_reproduces_reference_sampling(golden_dir):
+    """The sharded Born-rule read (distributed._sharded_sample) chains the
+    sequential cumsum shard to shard.  On the reference's own draws, every
+    split of the probability vector into 2..8 shards gives the reference's m:
+    the running sum entering a shard is exactly the one leaving the last."""
+    d = np.load(golden_dir / "sampling.npz")
+    p = oracle.probabilities(d["state"])
+    q = p.size
+    rng = np.random.default_rng(3)
+    for world in (2, 3, 4, 8):
+        cuts = [0] + sorted(rng.choice(np.arange(1, q), world - 1, replace=False).tolist()) + [q]
+        bounds, s = [], 0.0
+        for g in range(world):
+            s_out = oracle.cumsum_total_from(p[cuts[g]:cuts[g + 1]], s)
+            bounds.append((s, s_out))
+            s = s_out
+        assert s == np.cumsum(p)[-1]
+        for u, m in d["draws"]:
+            target = float(u) * s
+            owner = next(g for g in range(world) if bounds[g][1] > target)
+            got = cuts[owner] + oracle.cumsum_search_from(p[cuts[owner]:cuts[owner + 1]], bounds[owner][0], target)
+            assert min(got, q - 1) == int(m)
