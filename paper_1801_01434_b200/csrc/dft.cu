@@ -982,13 +982,18 @@ static int launch_dft_tc32_uniform(MmaArgs a, cudaStream_t st)
     return SHB_OK;
 }
 
-// FP32 fast path for the uniform comb: the BF16 tensor-core form (tiles == 1),
-// SHB_FP32_ENGINE=vector selects the FP32 Horner kernel instead.
-static bool use_tc32_engine()
+// FP32 fast path for the uniform comb (tiles == 1): the BF16 tensor-core
+// forms.  SHB_FP32_ENGINE=vector selects the FP32 Horner kernel, =mma the
+// warp-level mma.sync form, =tcgen05 the TMEM form (dft_tc05.cu).
+enum Fp32Engine { F32_VECTOR, F32_MMA, F32_TC05 };
+static Fp32Engine fp32_engine()
 {
     const char *e = getenv("SHB_FP32_ENGINE");
-    return !(e && e[0] == 'v');
+    if (e && e[0] == 'v') return F32_VECTOR;
+    if (e && e[0] == 't') return F32_TC05;
+    return F32_MMA;
 }
+static bool use_tc32_engine() { return fp32_engine() != F32_VECTOR; }
 
 // Engine choice for FP64, tiles == 1 (measured, profiles/r01_mma_real.jsonl):
 // * uniform comb and real amplitudes: the real-A DMMA form, 2 real products
@@ -1110,6 +1115,9 @@ extern "C" int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, ui
     a.out_im = amp_im * scale;
     cudaStream_t st = as_stream(stream);
     if (precision == SHB_FP32) {
+        if (tiles == 1 && length && fp32_engine() == F32_TC05)
+            return tc05_dft_uniform(length, a0, stride, q, c_begin, c_count, a.out_re, a.out_im, d_out, d_prob,
+                                    d_block_sums, (uint64_t)DFT_THREADS * Prec<float>::K, st);
         if (tiles == 1 && length && use_tc32_engine()) {
             MmaArgs m{nullptr, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
                       1.0, 0.0, a.out_re, a.out_im, (double2 *)d_out, d_prob, d_block_sums};
@@ -1135,7 +1143,7 @@ extern "C" const char *shb_dft_engine(int uniform, int real, uint64_t q, int pre
 {
     if (precision == SHB_FP32 && uniform && tiles == 1 && use_tc32_engine()) {
         if (flops_per_term) *flops_per_term = 8;  // 4 bf16 MACs: (Re, Im) x (hi, lo)
-        return "dft_tc32_uniform_kernel";
+        return fp32_engine() == F32_TC05 ? "dft_tc05_uniform_kernel" : "dft_tc32_uniform_kernel";
     }
     const bool mma = precision == SHB_FP64 && tiles == 1 && use_mma_engine(uniform != 0, q);
     const bool realf = mma && (uniform || real) && use_real_form();

@@ -1,0 +1,442 @@
+// FP32 fast path of the QFT on the 5th-generation tensor cores (tcgen05 +
+// TMEM): the uniform comb (the collapsed Shor register), precision SHB_FP32,
+// tiles == 1.  Same sum and the same GEMM factorisation as the mma.sync
+// kernels of dft.cu (qft.dense_dft, qft.py:95-112 / _kernels.py:16-30):
+//
+//   a_j = a0 + j*stride,  j = (sb*NB + jj)*BK + k   (super-block sb, row-block jj, k < BK)
+//   V_c = scale*amp * sum_sb sum_jj e^{+2 pi i (a0 + (sb*NB + jj)*BK*stride) c / q} * T[c, jj]
+//   T[c, jj] = sum_k G[c, k] * 1,   G[c, k] = e^{+2 pi i k stride c / q}
+//
+// One tcgen05.mma (M = 128 outputs, N = NB row-blocks, K = 16) multiplies the
+// generated phase matrix G (A operand, shared memory, K-major) by ones (B
+// operand, shared memory) into an FP32 accumulator in TMEM: each row-block's
+// T for 128 outputs at once.  G is split into two bf16 terms, G = G_hi + G_lo
+// (|G - G_hi - G_lo| <= 2^-18 |G|): 4 MMAs per k-step (Re/Im x hi/lo), the
+// same 4 bf16 multiply-adds per phase term as dft_tc32_uniform_kernel.
+//
+// Roles (one persistent CTA per SM, 9 warps):
+//  * warp 8, one elected thread: issues the MMAs of a super-block into one of
+//    two TMEM accumulator buffers and commits them to that buffer's `full`
+//    mbarrier;
+//  * warps 0-7 (two workers per TMEM lane = output): build G for the tile, then per
+//    super-block load the accumulators (tcgen05.ld 32x32b), release the
+//    buffer (`empty` mbarrier) and fold the NB row-blocks by an FP32 Horner
+//    with w^{-BK}, rotate by the exact-index seed of the last row-block
+//    (sincospif of the exact integer phase index) and add into an FP64 total.
+// The last super-block of a tile runs with N rounded up to a multiple of 8
+// row-blocks and a ones mask that zeroes amplitudes past the progression.
+#include <cuda_bf16.h>
+#include <math.h>
+#include <stdlib.h>
+
+#include "shb_internal.cuh"
+
+namespace shb {
+
+namespace tc05 {
+
+constexpr int TILE = 128;            // outputs per tile (MMA M, TMEM lanes)
+constexpr int NB = 64;               // row-blocks per super-block (MMA N)
+constexpr int BK = 128;              // k per row-block (MMA K total)
+constexpr int KSTEPS = BK / 16;      // tcgen05.mma K = 16 for bf16
+constexpr int SB_AMPS = NB * BK;     // amplitudes per super-block (8192)
+constexpr int A_BYTES = TILE * BK * 2;   // one bf16 variant of G: 32 KB
+constexpr int B_BYTES = NB * BK * 2;     // ones / mask: 16 KB
+constexpr int SMEM_BYTES = 4 * A_BYTES + 2 * B_BYTES + 1024;  // + alignment slack
+constexpr int TMEM_COLS = 512;       // [0, 256): 2 accumulator buffers x (Re NB | Im NB); [256, 512): A = G
+constexpr uint32_t A_COL = 256;      // 4 variants x BK/2 columns (bf16 pairs)
+constexpr int WORKERS = 256;         // 8 warps: G builders + folders (2 per TMEM lane quarter)
+constexpr int MMA_WARP = WORKERS / 32;
+constexpr int THREADS = WORKERS + 32;  // + 1 MMA warp
+constexpr uint32_t CORE_ROW_BYTES = 16;
+constexpr uint32_t LBO = 128;                    // next 8-wide k group
+constexpr uint32_t SBO = (BK / 8) * 128;         // next 8-row group
+
+// byte offset of (row, k) in a K-major no-swizzle operand: 8 x 16 B core
+// matrices, k groups adjacent (LBO), 8-row groups every SBO (validated by
+// scripts/tc05_probe.cu against a host GEMM)
+__device__ __forceinline__ uint32_t kmajor(int row, int k)
+{
+    return (uint32_t)(row >> 3) * SBO + (uint32_t)(k >> 3) * LBO + (uint32_t)(row & 7) * CORE_ROW_BYTES +
+           (uint32_t)(k & 7) * 2;
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr)
+{
+    return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(LBO >> 4) << 16) | ((uint64_t)(SBO >> 4) << 32) |
+           ((uint64_t)1 << 46);  // sm_100 descriptor version; no swizzle
+}
+
+// kind::f16 instruction descriptor: BF16 x BF16 -> F32, both K-major
+__device__ __forceinline__ uint32_t idesc(int n)
+{
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TILE >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void mma_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+
+__device__ __forceinline__ void commit(uint64_t *bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_addr(bar))
+                 : "memory");
+}
+
+// mbarrier wait that traps instead of hanging if the pipeline ever stalls
+__device__ __forceinline__ void wait_bar(uint64_t *bar, uint32_t phase)
+{
+    uint32_t ok = 0;
+    for (uint64_t spin = 0; !ok; spin++) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_addr(bar)), "r"(phase)
+            : "memory");
+        if (spin > (1ull << 28)) asm volatile("trap;");
+    }
+}
+
+__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16])
+{
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 16; i++) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void phase_f32(uint64_t idx, uint64_t q, double two_over_q, float &c, float &s)
+{
+    const int64_t sidx = (idx > (q >> 1)) ? (int64_t)(idx - q) : (int64_t)idx;
+    sincospif((float)((double)sidx * two_over_q), &s, &c);
+}
+
+struct Args {
+    uint64_t length, a0, stride, q;
+    double two_over_q;
+    uint64_t c_begin, c_count, ntiles;
+    double out_re, out_im;
+    double2 *out;
+    double *prob;
+    double *tile_sums;  // per tile sum of |V|^2 (nullable)
+};
+
+__global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args p)
+{
+    extern __shared__ unsigned char smem_raw[];
+    // 1024-B aligned operand region: A variants (Re hi, Re lo, Im hi, Im lo), ones, last-block mask
+    unsigned char *base = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    unsigned char *sA = base;
+    unsigned char *sOnes = base + 4 * A_BYTES;
+    unsigned char *sMask = sOnes + B_BYTES;
+    __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2], a_ready, a_free;
+    __shared__ uint32_t tmem_base_sh;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint64_t q = p.q, qmask = q - 1;
+    const uint64_t nsb = (p.length + SB_AMPS - 1) / SB_AMPS;
+    // the last super-block: valid row-blocks and the MMA N it runs with
+    const uint64_t last_amps = p.length - (nsb - 1) * SB_AMPS;  // in (0, SB_AMPS]
+    const int last_rb = (int)((last_amps + BK - 1) / BK);
+    const int last_n = ((last_rb + 7) / 8) * 8;
+
+    // ones and the last-super-block mask (B operands: row = row-block jj, K-major)
+    for (int i = tid; i < NB * BK; i += THREADS) {
+        const int jj = i / BK, k = i % BK;
+        const __nv_bfloat16 one = __float2bfloat16_rn(1.f), zero = __float2bfloat16_rn(0.f);
+        *reinterpret_cast<__nv_bfloat16 *>(sOnes + kmajor(jj, k)) = one;
+        *reinterpret_cast<__nv_bfloat16 *>(sMask + kmajor(jj, k)) =
+            ((uint64_t)jj * BK + k < last_amps) ? one : zero;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_addr(&tmem_base_sh)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        mbar_init(&full_bar[0], 1);
+        mbar_init(&full_bar[1], 1);
+        mbar_init(&empty_bar[0], WORKERS);
+        mbar_init(&empty_bar[1], WORKERS);
+        mbar_init(&a_ready, WORKERS);
+        mbar_init(&a_free, 1);
+        fence_mbar_init();
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == MMA_WARP) {
+        // ---------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            const uint32_t aaddr = smem_addr(sA), onesaddr = smem_addr(sOnes), maskaddr = smem_addr(sMask);
+            const uint32_t a_tmem = tmem + A_COL;
+            uint64_t g = 0;  // super-blocks issued so far (buffer g & 1)
+            uint32_t it = 0;
+            for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
+                wait_bar(&a_ready, it & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                // staged G -> TMEM A region: one 128x256b copy per (variant, k-step).
+                // tcgen05.cp and tcgen05.mma execute in issue order, so the copy
+                // lands after the previous tile's MMAs have read the old A
+#pragma unroll
+                for (int v = 0; v < 4; v++)
+#pragma unroll
+                    for (int s = 0; s < KSTEPS; s++)
+                        asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(a_tmem + v * (BK / 2) + s * 8),
+                                     "l"(smem_desc(aaddr + v * A_BYTES + s * 2 * LBO))
+                                     : "memory");
+                commit(&a_free);  // the staging buffer may be refilled once the copies are done
+                for (uint64_t sb = 0; sb < nsb; sb++, g++) {
+                    const uint32_t b = (uint32_t)(g & 1);
+                    if (g >= 2) wait_bar(&empty_bar[b], (uint32_t)((g >> 1) - 1) & 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const bool last = sb + 1 == nsb;
+                    const int n = last ? last_n : NB;
+                    const uint32_t id = idesc(n);
+                    const uint32_t bsrc = last ? maskaddr : onesaddr;
+                    const uint32_t d_re = tmem + b * (2 * NB), d_im = d_re + NB;
+#pragma unroll
+                    for (int s = 0; s < KSTEPS; s++) {
+                        const uint64_t db = smem_desc(bsrc + s * 2 * LBO);
+                        const uint32_t ak = a_tmem + s * 8;
+                        mma_ta(d_re, ak + 0 * (BK / 2), db, id, s > 0);
+                        mma_ta(d_re, ak + 1 * (BK / 2), db, id, 1);
+                        mma_ta(d_im, ak + 2 * (BK / 2), db, id, s > 0);
+                        mma_ta(d_im, ak + 3 * (BK / 2), db, id, 1);
+                    }
+                    commit(&full_bar[b]);
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------- G builders + folders (row = TMEM lane = output)
+        // worker w: row = w % 128 (warp w/32 reads TMEM lane quarter (w/32) % 4),
+        // half = w / 128 builds G columns [64 half, 64 half + 64) and folds
+        // row-blocks [n/2 half, n/2 (half + 1)) of every super-block
+        const int row = tid & (TILE - 1), half = tid >> 7;
+        const uint32_t lane_addr = (uint32_t)(32 * (warp & 3)) << 16;
+        __shared__ double vpart[2][TILE];
+        __shared__ double wsum[8];
+        uint64_t g = 0;
+        uint32_t it = 0;
+        // G[c, k] = e^{+2 pi i k stride c / q} for this worker's row and k half into
+        // the staging buffer: exact sincospif every 8 k, FP32 rotation in between,
+        // split into bf16 hi + lo
+        auto build_g = [&](uint64_t tt) {
+            const uint64_t cg = p.c_begin + tt * TILE + row;
+            {
+                float wr, wi;
+                phase_f32((p.stride * cg) & qmask, q, p.two_over_q, wr, wi);
+#pragma unroll 2
+                for (int k0 = half * (BK / 2); k0 < (half + 1) * (BK / 2); k0 += 8) {
+                    float gr, gi;
+                    phase_f32(((uint64_t)k0 * p.stride * cg) & qmask, q, p.two_over_q, gr, gi);
+                    uint32_t pk[4][4];
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        float v[2][2];  // [elem][re, im]
+#pragma unroll
+                        for (int u = 0; u < 2; u++) {
+                            v[u][0] = gr;
+                            v[u][1] = gi;
+                            const float nr = fmaf(gr, wr, -gi * wi), ni = fmaf(gr, wi, gi * wr);
+                            gr = nr;
+                            gi = ni;
+                        }
+                        const __nv_bfloat162 rh = __floats2bfloat162_rn(v[0][0], v[1][0]);
+                        const __nv_bfloat162 ih = __floats2bfloat162_rn(v[0][1], v[1][1]);
+                        const __nv_bfloat162 rl = __floats2bfloat162_rn(v[0][0] - __low2float(rh),
+                                                                         v[1][0] - __high2float(rh));
+                        const __nv_bfloat162 il = __floats2bfloat162_rn(v[0][1] - __low2float(ih),
+                                                                         v[1][1] - __high2float(ih));
+                        pk[0][e / 2] = *reinterpret_cast<const uint32_t *>(&rh);
+                        pk[1][e / 2] = *reinterpret_cast<const uint32_t *>(&rl);
+                        pk[2][e / 2] = *reinterpret_cast<const uint32_t *>(&ih);
+                        pk[3][e / 2] = *reinterpret_cast<const uint32_t *>(&il);
+                    }
+                    const uint32_t off = kmajor(row, k0);
+#pragma unroll
+                    for (int v4 = 0; v4 < 4; v4++)
+                        *reinterpret_cast<uint4 *>(sA + v4 * A_BYTES + off) =
+                            make_uint4(pk[v4][0], pk[v4][1], pk[v4][2], pk[v4][3]);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&a_ready);
+        };
+        if ((uint64_t)blockIdx.x < p.ntiles) build_g(blockIdx.x);
+        for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
+            const uint64_t c = p.c_begin + t * TILE + row;
+            // the next tile's G goes into the staging buffer as soon as the MMA
+            // warp has copied this tile's G into TMEM: it overlaps this tile's MMAs
+            if (t + gridDim.x < p.ntiles) {
+                wait_bar(&a_free, it & 1u);
+                build_g(t + gridDim.x);
+            }
+
+            // fold this worker's half of every super-block: h = h * W + T[jj] (FP32), W = w^{-BK}
+            float Wr, Wi;
+            {
+                float co, si;
+                phase_f32(((uint64_t)BK * p.stride * c) & qmask, q, p.two_over_q, co, si);
+                Wr = co;
+                Wi = -si;
+            }
+            double vr = 0.0, vi = 0.0;
+            for (uint64_t sb = 0; sb < nsb; sb++, g++) {
+                const uint32_t b = (uint32_t)(g & 1);
+                wait_bar(&full_bar[b], (uint32_t)(g >> 1) & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const int n = (sb + 1 == nsb) ? last_n : NB;
+                const int j_lo = half * (n / 2), j_hi = j_lo + n / 2;
+                const uint32_t d_re = tmem + lane_addr + b * (2 * NB), d_im = d_re + NB;
+                float hr = 0.f, hi = 0.f;
+                for (int j0 = j_lo; j0 < j_hi; j0 += 16) {
+                    float tr[16], ti[16];
+                    ld16(d_re + j0, tr);
+                    ld16(d_im + j0, ti);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (j0 + 16 >= j_hi) {  // this worker is done with the buffer
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        mbar_arrive(&empty_bar[b]);
+                    }
+                    const int cnt = j_hi - j0 < 16 ? j_hi - j0 : 16;
+#pragma unroll
+                    for (int e = 0; e < 16; e++) {
+                        if (e < cnt) {
+                            const float nr = fmaf(hr, Wr, fmaf(-hi, Wi, tr[e]));
+                            const float ni = fmaf(hr, Wi, fmaf(hi, Wr, ti[e]));
+                            hr = nr;
+                            hi = ni;
+                        }
+                    }
+                }
+                // seed of the last folded row-block: a0 + (sb*NB + j_hi-1)*BK*stride
+                const uint64_t a_last = p.a0 + ((sb * NB + (uint64_t)(j_hi - 1)) * BK) * p.stride;
+                float sc, ss;
+                phase_f32((a_last * c) & qmask, q, p.two_over_q, sc, ss);
+                vr = fma((double)sc, (double)hr, fma(-(double)ss, (double)hi, vr));
+                vi = fma((double)sc, (double)hi, fma((double)ss, (double)hr, vi));
+            }
+            // combine the two halves (fixed order: half 0 + half 1), then the
+            // epilogue: output factor, |V|^2 (hypot^2, as np.abs(.)**2), tile sum
+            if (half == 1) {
+                vpart[0][row] = vr;
+                vpart[1][row] = vi;
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(WORKERS) : "memory");
+            double pr = 0.0;
+            if (half == 0) {
+                vr += vpart[0][row];
+                vi += vpart[1][row];
+                const uint64_t ci = t * TILE + row;
+                if (ci < p.c_count) {
+                    const double o_re = vr * p.out_re - vi * p.out_im;
+                    const double o_im = vr * p.out_im + vi * p.out_re;
+                    p.out[ci] = make_double2(o_re, o_im);
+                    const double hh = hypot(o_re, o_im);
+                    pr = hh * hh;
+                    if (p.prob) p.prob[ci] = pr;
+                }
+            }
+            if (p.tile_sums) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) pr += __shfl_down_sync(0xffffffffu, pr, o);
+                if (lane == 0) wsum[warp] = pr;
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(WORKERS) : "memory");
+            if (p.tile_sums && tid == 0) p.tile_sums[t] = (wsum[0] + wsum[1]) + (wsum[2] + wsum[3]);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
+__global__ void tile_group_sums_kernel(const double *__restrict__ part, uint64_t nparts, int group,
+                                       double *__restrict__ out, uint64_t nout)
+{
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nout) return;
+    double s = 0.0;
+    for (int i = 0; i < group; i++) {
+        const uint64_t j = g * group + i;
+        if (j < nparts) s += part[j];
+    }
+    out[g] = s;
+}
+
+}  // namespace tc05
+
+// Caller contract as shb_dft_uniform (validated there); block sums in the
+// caller's shb_dft_num_blocks(c_count, SHB_FP32) layout (slot_outputs per slot).
+int tc05_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin,
+                     uint64_t c_count, double out_re, double out_im, double *d_out, double *d_prob,
+                     double *d_block_sums, uint64_t slot_outputs, cudaStream_t st)
+{
+    using namespace tc05;
+    if (length == 0 || c_count == 0) return set_error(SHB_EINVAL, "tc05 path needs a non-empty support and output");
+    Args a{};
+    a.length = length;
+    a.a0 = a0;
+    a.stride = stride;
+    a.q = q;
+    a.two_over_q = 2.0 / (double)q;
+    a.c_begin = c_begin;
+    a.c_count = c_count;
+    a.ntiles = (c_count + TILE - 1) / TILE;
+    a.out_re = out_re;
+    a.out_im = out_im;
+    a.out = (double2 *)d_out;
+    a.prob = d_prob;
+    Scratch part;
+    if (d_block_sums) {
+        SHB_TRY(scratch_alloc(part, sizeof(double) * a.ntiles, st));
+        a.tile_sums = (double *)part.ptr;
+    }
+    SHB_TRY_CUDA(cudaFuncSetAttribute(dft_tc05_uniform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES));
+    const uint64_t grid = a.ntiles < (uint64_t)sm_count() ? a.ntiles : (uint64_t)sm_count();
+    dft_tc05_uniform_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, st>>>(a);
+    SHB_LAUNCHED();
+    if (d_block_sums) {
+        const int group = (int)(slot_outputs / TILE);
+        const uint64_t nout = (c_count + slot_outputs - 1) / slot_outputs;
+        tile_group_sums_kernel<<<(unsigned)((nout + 255) / 256), 256, 0, st>>>((const double *)part.ptr,
+                                                                               a.ntiles, group, d_block_sums,
+                                                                               nout);
+        SHB_LAUNCHED();
+    }
+    SHB_TRY_CUDA(cudaGetLastError());
+    return SHB_OK;
+}
+
+}  // namespace shb

@@ -196,7 +196,7 @@ def test_fp32_fast_path(golden_dir):
     assert np.max(np.abs(pu32 - p64)) / p64.max() <= 1e-4
 
 
-@pytest.mark.parametrize("engine", ["vector", "tc"])
+@pytest.mark.parametrize("engine", ["vector", "mma", "tcgen05"])
 def test_fp32_engines_uniform_vs_oracle(engine, monkeypatch):
     """The FP32 fast path for a uniform comb: the FP32 Horner kernel and the
     BF16 tensor-core form (G = G_hi + G_lo, FP32 accumulation, FP64 segment
