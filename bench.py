@@ -380,11 +380,11 @@ def run_b200(args):
             "max_abs_dp_over_max_p": float(err[0] / err[1]), "tolerance": 1e-4,
             "m": rec32.m, "m_equal_fp64": rec32.m == rec.m, "kernel": f"shb::{k32}",
             "achieved_tflops": tf32, "flops_per_phase_term": f32.value,
-            "note": "DFT kernel only; not the headline (FP64).  The tensor-core form issues 4 bf16 MACs per "
-                    "phase term (Re/Im x hi/lo split of the phase matrix) on mma.sync m16n8k16; "
-                    "scripts/lowp_mma_probe.cu measures 540 TFLOP/s for that instruction on this GPU"}
+            "note": "DFT kernel only; not the headline (FP64).  The tensor-core forms issue 4 bf16 MACs per "
+                    "phase term (Re/Im x hi/lo split of the phase matrix): tcgen05.mma with TMEM "
+                    "accumulators (default) or mma.sync m16n8k16 (SHB_FP32_ENGINE=mma)"}
         peaks = _measured_peaks()
-        if peaks.get("bf16_tflops") and "tc32" in k32:
+        if peaks.get("bf16_tflops") and ("tc05" in k32 or "tc32" in k32):
             line["fp32_fast_path"]["frac_of_bf16_peak"] = tf32 / peaks["bf16_tflops"]
             line["fp32_fast_path"]["bf16_peak_source"] = "MEASURED_PEAKS.json bf16_tflops (cuBLAS, tcgen05)"
 

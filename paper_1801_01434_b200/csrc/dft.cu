@@ -983,15 +983,16 @@ static int launch_dft_tc32_uniform(MmaArgs a, cudaStream_t st)
 }
 
 // FP32 fast path for the uniform comb (tiles == 1): the BF16 tensor-core
-// forms.  SHB_FP32_ENGINE=vector selects the FP32 Horner kernel, =mma the
-// warp-level mma.sync form, =tcgen05 the TMEM form (dft_tc05.cu).
+// forms.  Default: the tcgen05/TMEM kernel (dft_tc05.cu; 1.3-1.8e14 phase
+// terms/s, scripts/tc05_check.py); SHB_FP32_ENGINE=mma selects the warp-level
+// mma.sync form (4e13), =vector the FP32 Horner kernel (7e12).
 enum Fp32Engine { F32_VECTOR, F32_MMA, F32_TC05 };
 static Fp32Engine fp32_engine()
 {
     const char *e = getenv("SHB_FP32_ENGINE");
     if (e && e[0] == 'v') return F32_VECTOR;
-    if (e && e[0] == 't') return F32_TC05;
-    return F32_MMA;
+    if (e && e[0] == 'm') return F32_MMA;
+    return F32_TC05;
 }
 static bool use_tc32_engine() { return fp32_engine() != F32_VECTOR; }
 

@@ -23,7 +23,7 @@
 //    buffer (`empty` mbarrier) and fold the NB row-blocks by an FP32 Horner
 //    with w^{-BK}, rotate by the exact-index seed of the last row-block
 //    (sincospif of the exact integer phase index) and add into an FP64 total.
-// The last super-block of a tile runs with N rounded up to a multiple of 8
+// The last super-block of a tile runs with N rounded up to a multiple of 32
 // row-blocks and a ones mask that zeroes amplitudes past the progression.
 #include <cuda_bf16.h>
 #include <math.h>
@@ -36,15 +36,15 @@ namespace shb {
 namespace tc05 {
 
 constexpr int TILE = 128;            // outputs per tile (MMA M, TMEM lanes)
-constexpr int NB = 64;               // row-blocks per super-block (MMA N)
+constexpr int NB = 128;              // row-blocks per super-block (MMA N: 128 reaches the full
+                                     // 4096 MAC/clk/SM, 64 only ~2800, scripts/tc05_rate_probe.cu)
 constexpr int BK = 128;              // k per row-block (MMA K total)
 constexpr int KSTEPS = BK / 16;      // tcgen05.mma K = 16 for bf16
-constexpr int SB_AMPS = NB * BK;     // amplitudes per super-block (8192)
+constexpr int SB_AMPS = NB * BK;     // amplitudes per super-block (16384)
 constexpr int A_BYTES = TILE * BK * 2;   // one bf16 variant of G: 32 KB
-constexpr int B_BYTES = NB * BK * 2;     // ones / mask: 16 KB
+constexpr int B_BYTES = NB * BK * 2;     // ones / mask: 32 KB
 constexpr int SMEM_BYTES = 4 * A_BYTES + 2 * B_BYTES + 1024;  // + alignment slack
-constexpr int TMEM_COLS = 512;       // [0, 256): 2 accumulator buffers x (Re NB | Im NB); [256, 512): A = G
-constexpr uint32_t A_COL = 256;      // 4 variants x BK/2 columns (bf16 pairs)
+constexpr int TMEM_COLS = 512;       // 2 accumulator buffers x (Re NB | Im NB)
 constexpr int WORKERS = 256;         // 8 warps: G builders + folders (2 per TMEM lane quarter)
 constexpr int MMA_WARP = WORKERS / 32;
 constexpr int THREADS = WORKERS + 32;  // + 1 MMA warp
@@ -81,15 +81,6 @@ __device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uin
         "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 
-// D[tmem] (+)= A[tmem] * B[smem]
-__device__ __forceinline__ void mma_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc)
-{
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
-}
-
 __device__ __forceinline__ void commit(uint64_t *bar)
 {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -112,16 +103,19 @@ __device__ __forceinline__ void wait_bar(uint64_t *bar, uint32_t phase)
     }
 }
 
-__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16])
+__device__ __forceinline__ void ld32(uint32_t taddr, float *v)
 {
-    uint32_t r[16];
+    uint32_t r[32];
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 #pragma unroll
-    for (int i = 0; i < 16; i++) v[i] = __uint_as_float(r[i]);
+    for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
 }
 
 __device__ __forceinline__ void phase_f32(uint64_t idx, uint64_t q, double two_over_q, float &c, float &s)
@@ -149,7 +143,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
     unsigned char *sA = base;
     unsigned char *sOnes = base + 4 * A_BYTES;
     unsigned char *sMask = sOnes + B_BYTES;
-    __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2], a_ready, a_free;
+    __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2], a_ready;
     __shared__ uint32_t tmem_base_sh;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -158,7 +152,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
     // the last super-block: valid row-blocks and the MMA N it runs with
     const uint64_t last_amps = p.length - (nsb - 1) * SB_AMPS;  // in (0, SB_AMPS]
     const int last_rb = (int)((last_amps + BK - 1) / BK);
-    const int last_n = ((last_rb + 7) / 8) * 8;
+    const int last_n = ((last_rb + 31) / 32) * 32;  // halves of whole 16-column TMEM loads
 
     // ones and the last-super-block mask (B operands: row = row-block jj, K-major)
     for (int i = tid; i < NB * BK; i += THREADS) {
@@ -180,7 +174,6 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
         mbar_init(&empty_bar[0], WORKERS);
         mbar_init(&empty_bar[1], WORKERS);
         mbar_init(&a_ready, WORKERS);
-        mbar_init(&a_free, 1);
         fence_mbar_init();
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -193,23 +186,11 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
         // ---------------------------------------------------------- MMA issuer
         if (lane == 0) {
             const uint32_t aaddr = smem_addr(sA), onesaddr = smem_addr(sOnes), maskaddr = smem_addr(sMask);
-            const uint32_t a_tmem = tmem + A_COL;
             uint64_t g = 0;  // super-blocks issued so far (buffer g & 1)
             uint32_t it = 0;
             for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
-                wait_bar(&a_ready, it & 1u);
+                wait_bar(&a_ready, it & 1u);  // G of this tile is in shared memory
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                // staged G -> TMEM A region: one 128x256b copy per (variant, k-step).
-                // tcgen05.cp and tcgen05.mma execute in issue order, so the copy
-                // lands after the previous tile's MMAs have read the old A
-#pragma unroll
-                for (int v = 0; v < 4; v++)
-#pragma unroll
-                    for (int s = 0; s < KSTEPS; s++)
-                        asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(a_tmem + v * (BK / 2) + s * 8),
-                                     "l"(smem_desc(aaddr + v * A_BYTES + s * 2 * LBO))
-                                     : "memory");
-                commit(&a_free);  // the staging buffer may be refilled once the copies are done
                 for (uint64_t sb = 0; sb < nsb; sb++, g++) {
                     const uint32_t b = (uint32_t)(g & 1);
                     if (g >= 2) wait_bar(&empty_bar[b], (uint32_t)((g >> 1) - 1) & 1u);
@@ -222,11 +203,11 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
 #pragma unroll
                     for (int s = 0; s < KSTEPS; s++) {
                         const uint64_t db = smem_desc(bsrc + s * 2 * LBO);
-                        const uint32_t ak = a_tmem + s * 8;
-                        mma_ta(d_re, ak + 0 * (BK / 2), db, id, s > 0);
-                        mma_ta(d_re, ak + 1 * (BK / 2), db, id, 1);
-                        mma_ta(d_im, ak + 2 * (BK / 2), db, id, s > 0);
-                        mma_ta(d_im, ak + 3 * (BK / 2), db, id, 1);
+                        const uint32_t koff = s * 2 * LBO;
+                        mma(d_re, smem_desc(aaddr + 0 * A_BYTES + koff), db, id, s > 0);
+                        mma(d_re, smem_desc(aaddr + 1 * A_BYTES + koff), db, id, 1);
+                        mma(d_im, smem_desc(aaddr + 2 * A_BYTES + koff), db, id, s > 0);
+                        mma(d_im, smem_desc(aaddr + 3 * A_BYTES + koff), db, id, 1);
                     }
                     commit(&full_bar[b]);
                 }
@@ -244,9 +225,9 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
         __shared__ double wsum[8];
         uint64_t g = 0;
         uint32_t it = 0;
-        // G[c, k] = e^{+2 pi i k stride c / q} for this worker's row and k half into
-        // the staging buffer: exact sincospif every 8 k, FP32 rotation in between,
-        // split into bf16 hi + lo
+        // G[c, k] = e^{+2 pi i k stride c / q} for this worker's row and k half
+        // (A operand in shared memory): exact sincospif every 8 k, FP32 rotation
+        // in between, split into bf16 hi + lo
         auto build_g = [&](uint64_t tt) {
             const uint64_t cg = p.c_begin + tt * TILE + row;
             {
@@ -289,15 +270,11 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(&a_ready);
         };
-        if ((uint64_t)blockIdx.x < p.ntiles) build_g(blockIdx.x);
         for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
             const uint64_t c = p.c_begin + t * TILE + row;
-            // the next tile's G goes into the staging buffer as soon as the MMA
-            // warp has copied this tile's G into TMEM: it overlaps this tile's MMAs
-            if (t + gridDim.x < p.ntiles) {
-                wait_bar(&a_free, it & 1u);
-                build_g(t + gridDim.x);
-            }
+            // the MMAs reading the previous tile's G are complete: this worker
+            // waited on the commit of that tile's last super-block
+            build_g(t);
 
             // fold this worker's half of every super-block: h = h * W + T[jj] (FP32), W = w^{-BK}
             float Wr, Wi;
@@ -315,25 +292,26 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
                 const int n = (sb + 1 == nsb) ? last_n : NB;
                 const int j_lo = half * (n / 2), j_hi = j_lo + n / 2;
                 const uint32_t d_re = tmem + lane_addr + b * (2 * NB), d_im = d_re + NB;
+                // all of this worker's accumulators in one burst of TMEM loads, then
+                // the buffer goes straight back to the MMA warp; the Horner runs
+                // from registers (columns past j_hi are loaded and ignored)
+                float tr[NB / 2], ti[NB / 2];
+                ld32(d_re + j_lo, tr);
+                ld32(d_re + j_lo + 32, tr + 32);
+                ld32(d_im + j_lo, ti);
+                ld32(d_im + j_lo + 32, ti + 32);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(&empty_bar[b]);
+                const int cnt = j_hi - j_lo;
                 float hr = 0.f, hi = 0.f;
-                for (int j0 = j_lo; j0 < j_hi; j0 += 16) {
-                    float tr[16], ti[16];
-                    ld16(d_re + j0, tr);
-                    ld16(d_im + j0, ti);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (j0 + 16 >= j_hi) {  // this worker is done with the buffer
-                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                        mbar_arrive(&empty_bar[b]);
-                    }
-                    const int cnt = j_hi - j0 < 16 ? j_hi - j0 : 16;
 #pragma unroll
-                    for (int e = 0; e < 16; e++) {
-                        if (e < cnt) {
-                            const float nr = fmaf(hr, Wr, fmaf(-hi, Wi, tr[e]));
-                            const float ni = fmaf(hr, Wi, fmaf(hi, Wr, ti[e]));
-                            hr = nr;
-                            hi = ni;
-                        }
+                for (int e = 0; e < NB / 2; e++) {
+                    if (e < cnt) {
+                        const float nr = fmaf(hr, Wr, fmaf(-hi, Wi, tr[e]));
+                        const float ni = fmaf(hr, Wi, fmaf(hi, Wr, ti[e]));
+                        hr = nr;
+                        hi = ni;
                     }
                 }
                 // seed of the last folded row-block: a0 + (sb*NB + j_hi-1)*BK*stride

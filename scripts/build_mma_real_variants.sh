@@ -13,7 +13,7 @@ build_one() {
     -DSHB_MMA_BU=$1 -DSHB_MMA_CT=$2 -DSHB_MMA_MINB_U=$3 -DSHB_MMA_SEG=$4 -DSHB_MMA_PIPE=$5 -DSHB_MMA_GREC=$6 -DSHB_MMA_NACC=$7 -DSHB_MMA_WARPS_U=$8 \
     -I include -c paper_1801_01434_b200/csrc/dft.cu -o /tmp/mrv_dft_$tag.o -Xptxas -v 2> /tmp/mrv_$tag.ptxas
   objs="/tmp/mrv_dft_$tag.o"
-  for src in capi modexp collapse sample context; do objs="$objs paper_1801_01434_b200/_obj/$src.o"; done
+  for src in capi modexp collapse sample context dft_tc05; do objs="$objs paper_1801_01434_b200/_obj/$src.o"; done
   nvcc -gencode arch=compute_100a,code=sm_100a -shared $objs -o $out -lcudart
   echo "built $out: $(grep -A2 'dft_mma_kernelILb1ELb1' /tmp/mrv_$tag.ptxas | grep -oE 'Used [0-9]+ registers|[0-9]+ bytes spill stores' | tr '\n' ' ')"
 }

@@ -11,7 +11,7 @@ build_one() {
     -DSHB_TC_BK=$1 -DSHB_TC_MINB=$2 -DSHB_TC_SEG=$3 \
     -I include -c paper_1801_01434_b200/csrc/dft.cu -o /tmp/tcv_dft_$tag.o -Xptxas -v 2> /tmp/tcv_$tag.ptxas
   objs="/tmp/tcv_dft_$tag.o"
-  for src in capi modexp collapse sample context; do objs="$objs paper_1801_01434_b200/_obj/$src.o"; done
+  for src in capi modexp collapse sample context dft_tc05; do objs="$objs paper_1801_01434_b200/_obj/$src.o"; done
   nvcc -gencode arch=compute_100a,code=sm_100a -shared $objs -o $out -lcudart
   echo "built $out: $(grep -A2 'dft_tc32' /tmp/tcv_$tag.ptxas | grep -oE 'Used [0-9]+ registers|[0-9]+ bytes spill stores' | tr '\n' ' ')"
 }

@@ -6,7 +6,7 @@ for v in "256 4" "256 2" "128 4" "128 8" "512 2"; do
   set -- $v
   out=paper_1801_01434_b200/_variants/libshorb200_T$1_K$2.so
   objs=""
-  for src in capi modexp collapse dft sample; do
+  for src in capi modexp collapse dft dft_tc05 sample context; do
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC \
       -DSHB_DFT_THREADS=$1 -DSHB_DFT_K64=$2 -I include -c paper_1801_01434_b200/csrc/$src.cu \
       -o /tmp/var_$src.o

@@ -126,7 +126,7 @@ def test_dft_engine_choice(lib, monkeypatch):
     assert eng(0, 1) == ("dft_mma_kernel<generic, real A>", 4)
     assert eng(0, 0) == ("dft_mma_kernel<generic, complex A>", 8)
     assert eng(1, 1, tiles=4)[0] == "dft_kernel<uniform>"
-    assert eng(1, 1, prec=nat.FP32) == ("dft_tc32_uniform_kernel", 8)
+    assert eng(1, 1, prec=nat.FP32) == ("dft_tc05_uniform_kernel", 8)
     assert eng(0, 1, prec=nat.FP32)[0] == "dft_kernel<generic>"
     # the choice never depends on the output range, only on q and the data
     assert eng(1, 1, q=1 << 8) == eng(1, 1, q=1 << 32)
@@ -135,5 +135,7 @@ def test_dft_engine_choice(lib, monkeypatch):
     monkeypatch.setenv("SHB_DFT_ENGINE", "mma")
     monkeypatch.setenv("SHB_MMA_REAL", "0")
     assert eng(1, 1) == ("dft_mma_kernel<uniform, complex A>", 8)
+    monkeypatch.setenv("SHB_FP32_ENGINE", "mma")
+    assert eng(1, 1, prec=nat.FP32)[0] == "dft_tc32_uniform_kernel"
     monkeypatch.setenv("SHB_FP32_ENGINE", "vector")
     assert eng(1, 1, prec=nat.FP32)[0] == "dft_kernel<uniform>"
