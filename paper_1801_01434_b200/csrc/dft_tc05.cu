@@ -38,12 +38,23 @@ namespace tc05 {
 constexpr int TILE = 128;            // outputs per tile (MMA M, TMEM lanes)
 constexpr int NB = 128;              // row-blocks per super-block (MMA N: 128 reaches the full
                                      // 4096 MAC/clk/SM, 64 only ~2800, scripts/tc05_rate_probe.cu)
-constexpr int BK = 128;              // k per row-block (MMA K total)
+#ifndef SHB_TC05_BK
+#define SHB_TC05_BK 128
+#endif
+constexpr int BK = SHB_TC05_BK;      // k per row-block (MMA K total)
+#ifndef SHB_TC05_CHAINS
+#define SHB_TC05_CHAINS 1
+#endif
+constexpr int HORNER_CHAINS = SHB_TC05_CHAINS;  // fold: 1 chain of 64, or 4 of 16
 constexpr int KSTEPS = BK / 16;      // tcgen05.mma K = 16 for bf16
-constexpr int SB_AMPS = NB * BK;     // amplitudes per super-block (16384)
-constexpr int A_BYTES = TILE * BK * 2;   // one bf16 variant of G: 32 KB
-constexpr int B_BYTES = NB * BK * 2;     // ones / mask: 32 KB
-constexpr int SMEM_BYTES = 4 * A_BYTES + 2 * B_BYTES + 1024;  // + alignment slack
+constexpr int SB_AMPS = NB * BK;     // amplitudes per super-block (8192)
+constexpr int A_BYTES = TILE * BK * 2;   // one bf16 variant of G
+constexpr int G_BYTES = 4 * A_BYTES;     // one tile's G (Re hi, Re lo, Im hi, Im lo)
+constexpr int B_BYTES = NB * BK * 2;     // ones / mask
+// two G buffers when they fit (BK = 64: the next tile's G is built while this
+// tile's MMAs run); at BK = 128 one buffer, rebuilt between tiles
+constexpr int G_BUFS = (2 * 4 * TILE * BK * 2 + 2 * NB * BK * 2 + 1024 <= 227 * 1024) ? 2 : 1;
+constexpr int SMEM_BYTES = G_BUFS * G_BYTES + 2 * B_BYTES + 1024;  // + alignment slack
 constexpr int TMEM_COLS = 512;       // 2 accumulator buffers x (Re NB | Im NB)
 constexpr int WORKERS = 256;         // 8 warps: G builders + folders (2 per TMEM lane quarter)
 constexpr int MMA_WARP = WORKERS / 32;
@@ -137,11 +148,12 @@ struct Args {
 __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args p)
 {
     extern __shared__ unsigned char smem_raw[];
-    // 1024-B aligned operand region: A variants (Re hi, Re lo, Im hi, Im lo), ones, last-block mask
+    // 1024-B aligned operand region: two tiles' G (A operand: Re hi, Re lo, Im hi,
+    // Im lo), ones, last-block mask
     unsigned char *base = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;
-    unsigned char *sOnes = base + 4 * A_BYTES;
+    unsigned char *sOnes = base + G_BUFS * G_BYTES;
     unsigned char *sMask = sOnes + B_BYTES;
     __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2], a_ready;
     __shared__ uint32_t tmem_base_sh;
@@ -191,6 +203,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
             for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
                 wait_bar(&a_ready, it & 1u);  // G of this tile is in shared memory
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t ga = aaddr + (G_BUFS == 2 ? (it & 1u) * G_BYTES : 0u);
                 for (uint64_t sb = 0; sb < nsb; sb++, g++) {
                     const uint32_t b = (uint32_t)(g & 1);
                     if (g >= 2) wait_bar(&empty_bar[b], (uint32_t)((g >> 1) - 1) & 1u);
@@ -204,10 +217,10 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
                     for (int s = 0; s < KSTEPS; s++) {
                         const uint64_t db = smem_desc(bsrc + s * 2 * LBO);
                         const uint32_t koff = s * 2 * LBO;
-                        mma(d_re, smem_desc(aaddr + 0 * A_BYTES + koff), db, id, s > 0);
-                        mma(d_re, smem_desc(aaddr + 1 * A_BYTES + koff), db, id, 1);
-                        mma(d_im, smem_desc(aaddr + 2 * A_BYTES + koff), db, id, s > 0);
-                        mma(d_im, smem_desc(aaddr + 3 * A_BYTES + koff), db, id, 1);
+                        mma(d_re, smem_desc(ga + 0 * A_BYTES + koff), db, id, s > 0);
+                        mma(d_re, smem_desc(ga + 1 * A_BYTES + koff), db, id, 1);
+                        mma(d_im, smem_desc(ga + 2 * A_BYTES + koff), db, id, s > 0);
+                        mma(d_im, smem_desc(ga + 3 * A_BYTES + koff), db, id, 1);
                     }
                     commit(&full_bar[b]);
                 }
@@ -226,10 +239,11 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
         uint64_t g = 0;
         uint32_t it = 0;
         // G[c, k] = e^{+2 pi i k stride c / q} for this worker's row and k half
-        // (A operand in shared memory): exact sincospif every 8 k, FP32 rotation
-        // in between, split into bf16 hi + lo
-        auto build_g = [&](uint64_t tt) {
+        // into G buffer `buf` (A operand in shared memory): exact sincospif every
+        // 8 k, FP32 rotation in between, split into bf16 hi + lo
+        auto build_g = [&](uint64_t tt, uint32_t buf) {
             const uint64_t cg = p.c_begin + tt * TILE + row;
+            unsigned char *gA = sA + buf * G_BYTES;
             {
                 float wr, wi;
                 phase_f32((p.stride * cg) & qmask, q, p.two_over_q, wr, wi);
@@ -263,26 +277,30 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
                     const uint32_t off = kmajor(row, k0);
 #pragma unroll
                     for (int v4 = 0; v4 < 4; v4++)
-                        *reinterpret_cast<uint4 *>(sA + v4 * A_BYTES + off) =
+                        *reinterpret_cast<uint4 *>(gA + v4 * A_BYTES + off) =
                             make_uint4(pk[v4][0], pk[v4][1], pk[v4][2], pk[v4][3]);
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(&a_ready);
         };
+        if (G_BUFS == 2 && (uint64_t)blockIdx.x < p.ntiles) build_g(blockIdx.x, 0);
         for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
             const uint64_t c = p.c_begin + t * TILE + row;
-            // the MMAs reading the previous tile's G are complete: this worker
-            // waited on the commit of that tile's last super-block
-            build_g(t);
+            // one buffer: the MMAs reading the previous tile's G are complete
+            // (this worker waited on the commit of that tile's last super-block)
+            if (G_BUFS == 1) build_g(t, 0);
 
             // fold this worker's half of every super-block: h = h * W + T[jj] (FP32), W = w^{-BK}
-            float Wr, Wi;
+            float Wr, Wi, W16r, W16i;
             {
                 float co, si;
                 phase_f32(((uint64_t)BK * p.stride * c) & qmask, q, p.two_over_q, co, si);
                 Wr = co;
                 Wi = -si;
+                phase_f32(((uint64_t)16 * BK * p.stride * c) & qmask, q, p.two_over_q, co, si);
+                W16r = co;
+                W16i = -si;
             }
             double vr = 0.0, vi = 0.0;
             for (uint64_t sb = 0; sb < nsb; sb++, g++) {
@@ -303,15 +321,42 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&empty_bar[b]);
-                const int cnt = j_hi - j_lo;
                 float hr = 0.f, hi = 0.f;
+                if (HORNER_CHAINS == 1) {
+                    const int cnt = j_hi - j_lo;
 #pragma unroll
-                for (int e = 0; e < NB / 2; e++) {
-                    if (e < cnt) {
-                        const float nr = fmaf(hr, Wr, fmaf(-hi, Wi, tr[e]));
-                        const float ni = fmaf(hr, Wi, fmaf(hi, Wr, ti[e]));
-                        hr = nr;
-                        hi = ni;
+                    for (int e = 0; e < NB / 2; e++) {
+                        if (e < cnt) {
+                            const float nr = fmaf(hr, Wr, fmaf(-hi, Wi, tr[e]));
+                            const float ni = fmaf(hr, Wi, fmaf(hi, Wr, ti[e]));
+                            hr = nr;
+                            hi = ni;
+                        }
+                    }
+                } else {
+                    // 4 independent chains of 16 row-blocks (ILP), joined with W^16:
+                    // h = ((h0 W^16 + h1) W^16 + h2) W^16 + h3
+                    const int nch = (j_hi - j_lo) / 16;  // halves are whole multiples of 16
+                    float cr[4] = {0.f, 0.f, 0.f, 0.f}, ci[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int e = 0; e < 16; e++)
+#pragma unroll
+                        for (int ch = 0; ch < 4; ch++) {
+                            const float nr = fmaf(cr[ch], Wr, fmaf(-ci[ch], Wi, tr[ch * 16 + e]));
+                            const float ni = fmaf(cr[ch], Wi, fmaf(ci[ch], Wr, ti[ch * 16 + e]));
+                            cr[ch] = nr;
+                            ci[ch] = ni;
+                        }
+                    hr = cr[0];
+                    hi = ci[0];
+#pragma unroll
+                    for (int ch = 1; ch < 4; ch++) {
+                        if (ch < nch) {
+                            const float nr = fmaf(hr, W16r, fmaf(-hi, W16i, cr[ch]));
+                            const float ni = fmaf(hr, W16i, fmaf(hi, W16r, ci[ch]));
+                            hr = nr;
+                            hi = ni;
+                        }
                     }
                 }
                 // seed of the last folded row-block: a0 + (sb*NB + j_hi-1)*BK*stride
@@ -320,6 +365,10 @@ __global__ void __launch_bounds__(THREADS, 1) dft_tc05_uniform_kernel(const Args
                 phase_f32((a_last * c) & qmask, q, p.two_over_q, sc, ss);
                 vr = fma((double)sc, (double)hr, fma(-(double)ss, (double)hi, vr));
                 vi = fma((double)sc, (double)hi, fma((double)ss, (double)hr, vi));
+                // the next tile's G, into the other buffer, while this tile's MMAs
+                // run (that buffer's last readers, the previous tile's MMAs, are
+                // complete: this worker waited on their commit)
+                if (G_BUFS == 2 && sb == 0 && t + gridDim.x < p.ntiles) build_g(t + gridDim.x, (it + 1) & 1u);
             }
             // combine the two halves (fixed order: half 0 + half 1), then the
             // epilogue: output factor, |V|^2 (hypot^2, as np.abs(.)**2), tile sum

@@ -1,0 +1,37 @@
+"""tcgen05 FP32 DFT variants (scripts/build_tc05_variants.sh): time and accuracy
+against the FP64 spectrum at q = 2^24 and q = 2^30 (uniform combs)."""
+import json
+import math
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+from paper_1801_01434_b200 import _native as nat  # noqa: E402
+from paper_1801_01434_b200 import device as dev  # noqa: E402
+
+libs = sorted(Path(nat.LIB_PATH.parent / "_variants").glob("*.so")) + [nat.LIB_PATH]
+for q, c0, r, M in [(1 << 24, 29, 116, 144631), (1 << 30, 10943, 16020, 67025)]:
+    amp = complex(1 / math.sqrt(M))
+    nat._lib = nat.load(nat.LIB_PATH)
+    _, p64, _ = dev.dft_uniform(amp, M, c0, r, q, 0, q, precision="fp64")
+    pmax = float(p64.max())
+    for so in libs:
+        nat._lib = nat.load(so)
+        fn = lambda: dev.dft_uniform(amp, M, c0, r, q, 0, q, precision="fp32")  # noqa: E731
+        o = fn()
+        del o
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out, p32, bs = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        print(json.dumps({"q": f"2^{q.bit_length() - 1}", "lib": so.name, "ms": round(ms, 2),
+                          "Gterms/s": round(q * M / ms / 1e6, 1), "TFLOPs_bf16": round(8 * q * M / ms / 1e9, 1),
+                          "max_dp_over_max_p": float((p32 - p64).abs().max()) / pmax}), flush=True)
+        del out, p32, bs
+        torch.cuda.empty_cache()
