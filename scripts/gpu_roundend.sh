@@ -8,6 +8,7 @@ timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_fi
 cat gpurun_out/bench_final.json; tail -3 gpurun_out/bench_final.err
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_final.json 2> gpurun_out/bench_ref_final.err; echo ref=$?
 cat gpurun_out/bench_ref_final.json
+[ -n "$SHB_TRACES" ] || exit 0
 rm -f gpurun_out/traces_large.jsonl
 for cfg in "32399 8" "32399 2" "32399 0" "46927 0"; do
   timeout 1200 python scripts/run_config.py $cfg >> gpurun_out/traces_large.jsonl 2>> gpurun_out/traces_large.err; echo "cfg $cfg rc=$?"
