@@ -421,7 +421,10 @@ struct MmaShape {
 #define SHB_MMA_NACC 1  // accumulator sets by k-step parity (real form)
 #endif
 #ifndef SHB_MMA_PIPE
-#define SHB_MMA_PIPE 0  // 2-set software pipeline over blocks
+#define SHB_MMA_PIPE 0  // 2-set software pipeline over blocks (amplitude-stream path)
+#endif
+#ifndef SHB_MMA_PIPE_U
+#define SHB_MMA_PIPE_U 1  // ... on the uniform path (+1.5 % at B = 128, scripts/build_mma_real_variants.sh)
 #endif
 #ifndef SHB_MMA_GREC
 #define SHB_MMA_GREC 1  // G fragments by recurrence from 2 exact phases
@@ -474,7 +477,7 @@ __global__ void __launch_bounds__(MmaShape<UNIF>::THREADS, MmaShape<UNIF>::MINB)
     constexpr int BPC = MMA_CHUNK / MMA_BLOCK > 0 ? MMA_CHUNK / MMA_BLOCK : 1;  // blocks per smem stage
     static_assert(UNIF || MMA_CHUNK % MMA_BLOCK == 0, "smem stages must hold whole blocks");
     constexpr int NACC = REALA ? SHB_MMA_NACC : 1;
-    constexpr int NP = SHB_MMA_PIPE ? 2 : 1;
+    constexpr int NP = (UNIF ? SHB_MMA_PIPE_U : SHB_MMA_PIPE) ? 2 : 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *buf = reinterpret_cast<double2 *>(smem_raw);
     __shared__ __align__(8) uint64_t full_bar[DFT_STAGES];

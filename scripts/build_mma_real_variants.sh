@@ -17,7 +17,7 @@ build_one() {
   nvcc -gencode arch=compute_100a,code=sm_100a -shared $objs -o $out -lcudart
   echo "built $out: $(grep -A2 'dft_mma_kernelILb1ELb1' /tmp/mrv_$tag.ptxas | grep -oE 'Used [0-9]+ registers|[0-9]+ bytes spill stores' | tr '\n' ' ')"
 }
-for v in ${VARIANTS:-"128 1 1 32768 0 1 1 8" "128 1 1 32768 0 1 1 4" "128 1 2 32768 0 1 1 4" "64 1 1 32768 0 1 1 4"}; do
+for v in "128 1 1 32768 1 1 1 8" "128 1 1 32768 1 1 2 8" "112 1 1 32768 1 1 1 8" "128 1 1 65536 0 1 1 8"; do
   build_one $v &
 done
 wait
