@@ -205,14 +205,15 @@ def test_fp32_engines_uniform_vs_oracle(engine, monkeypatch):
     block, M < one block), output shards and a q = 2^24 comb."""
     monkeypatch.setenv("SHB_FP32_ENGINE", engine)
     amp = 0.3 - 0.1j
-    for q, c0, r, M in [(1 << 10, 5, 3, 1), (1 << 10, 5, 3, 255), (1 << 12, 1, 7, 585), (1 << 16, 11, 12, 5461),
-                        (1 << 20, 3, 1, (1 << 20) - 3), (1 << 24, 29, 116, 144631)]:
+    for q, c0, r, M in [(2, 1, 1, 1), (4, 0, 1, 4), (8, 3, 2, 3), (1 << 10, 5, 3, 1), (1 << 10, 5, 3, 255),
+                        (1 << 12, 1, 7, 585), (1 << 16, 11, 12, 5461), (1 << 20, 3, 1, (1 << 20) - 3),
+                        (1 << 24, 29, 116, 144631)]:
         rows = np.unique(np.concatenate([np.arange(0, min(q, 4096)), np.arange(q - 130, q),
                                          np.random.default_rng(q).integers(0, q, 2000)])).astype(np.uint64)
         supp = c0 + r * np.arange(M, dtype=np.uint64)
         ref = oracle.dft_rows(supp, np.full(M, amp), q, rows)
         pref = np.abs(ref) ** 2
-        for lo, cnt in [(0, q), (77, min(q - 77, 129)), (q - 130, 130)]:
+        for lo, cnt in ([(0, q), (77, min(q - 77, 129)), (q - 130, 130)] if q > 256 else [(0, q), (1, q - 1)]):
             out, prob, bs = dev.dft_uniform(amp, M, c0, r, q, lo, cnt, precision="fp32")
             sel = (rows >= lo) & (rows < lo + cnt)
             o = out.cpu().numpy().view(np.complex128)[(rows[sel] - lo).astype(np.int64)]
@@ -609,11 +610,12 @@ def test_both_fp64_engines_vs_oracle(engine, real_form, monkeypatch):
     monkeypatch.setenv("SHB_DFT_ENGINE", engine)
     monkeypatch.setenv("SHB_MMA_REAL", real_form)
     rng = np.random.default_rng(21)
-    for q, c0, r, M in [(1 << 10, 5, 3, 1), (1 << 10, 5, 3, 255), (1 << 12, 1, 7, 585), (1 << 16, 11, 12, 5461)]:
+    for q, c0, r, M in [(2, 1, 1, 1), (8, 3, 2, 3), (1 << 10, 5, 3, 1), (1 << 10, 5, 3, 255), (1 << 12, 1, 7, 585),
+                        (1 << 16, 11, 12, 5461)]:
         supp = c0 + r * np.arange(M, dtype=np.uint64)
         amps_h = rng.standard_normal(M) + 1j * rng.standard_normal(M)
         amps = torch.from_numpy(amps_h.view(np.float64)).cuda()
-        for lo, cnt in [(0, q), (77, 129), (q - 130, 130)]:
+        for lo, cnt in ([(0, q), (77, 129), (q - 130, 130)] if q > 256 else [(0, q), (1, q - 1)]):
             rows = np.arange(lo, lo + cnt, dtype=np.uint64)
             out, prob, bs = dev.dft(amps, M, c0, r, q, lo, cnt)
             ref = oracle.dft_rows(supp, amps_h, q, rows)
