@@ -342,11 +342,12 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": el_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
         "data": "synthetic (the register is generated by the algorithm from n and the seed)",
-        "config": {"workload": f"n={args.n} (179x181) q=2^{q.bit_length() - 1} seed={args.seed} "
+        "config": {"workload": f"n={args.n}{_factor_label(outcome)} q=2^{q.bit_length() - 1} seed={args.seed} "
                                f"x={x} r={rec.r} M={M}: one full attempt per step",
                    "n": args.n, "q": q, "x": x, "k": rec.k, "r": rec.r, "M": M, "m": rec.m,
                    "precision": args.precision, "parallelism": f"c/a-sharded x{world}",
-                   "l2": "no flush needed: each step writes 24 GiB (spectrum + |V|^2) >> 126 MB L2",
+                   "l2": f"no flush needed: each step writes {24 * q / 2**30:.3g} GiB (spectrum + |V|^2) "
+                         f"{'>>' if 24 * q > 4 * 126e6 else 'vs'} the 126 MB L2",
                    "outcome": outcome.kind, "factors": list(outcome.factors) if outcome.factors else None},
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -416,6 +417,11 @@ def run_b200(args):
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def _factor_label(outcome) -> str:
+    f = getattr(outcome, "factors", None)
+    return f" ({'x'.join(str(v) for v in f)})" if f else ""
 
 
 def _measured_peaks() -> dict:
