@@ -17,7 +17,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libshorb200.so"
-SOURCES = ["capi.cu", "modexp.cu", "collapse.cu", "dft.cu", "dft_tc05.cu", "sample.cu", "context.cu"]
+SOURCES = ["capi.cu", "modexp.cu", "collapse.cu", "dft.cu", "dft_tc05.cu", "dft_i8.cu", "sample.cu", "context.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-O2", "-Xptxas", "-v"]

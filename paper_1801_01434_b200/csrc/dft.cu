@@ -1015,8 +1015,16 @@ static bool use_mma_engine(bool uniform, uint64_t q)
     (void)uniform;
     (void)q;
     const char *e = getenv("SHB_DFT_ENGINE");
-    if (e && e[0]) return e[0] == 'm';
+    if (e && e[0]) return e[0] == 'm' || e[0] == 'i';  // i8 serves the uniform comb only
     return true;
+}
+
+// FP64-accurate uniform comb on the int8 tensor cores (dft_i8.cu): exact
+// integer products of an 8-digit split of G*2^55.  SHB_DFT_ENGINE=i8.
+static bool use_i8_engine()
+{
+    const char *e = getenv("SHB_DFT_ENGINE");
+    return e && e[0] == 'i';
 }
 
 static bool use_real_form()
@@ -1129,6 +1137,9 @@ extern "C" int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, ui
         }
         return launch_dft<float, true>(a, length, tiles, st);
     }
+    if (tiles == 1 && length && use_i8_engine())
+        return i8_dft_uniform(length, a0, stride, q, c_begin, c_count, a.out_re, a.out_im, d_out, d_prob,
+                              d_block_sums, (uint64_t)DFT_THREADS * Prec<double>::K, st);
     if (tiles == 1 && length && use_mma_engine(true, q)) {
         // the amplitude is factored out (out factor = amp*scale): the MMA runs on ones
         MmaArgs m{nullptr, length, a0, stride, q, 2.0 / (double)q, c_begin, c_count,
@@ -1148,6 +1159,10 @@ extern "C" const char *shb_dft_engine(int uniform, int real, uint64_t q, int pre
     if (precision == SHB_FP32 && uniform && tiles == 1 && use_tc32_engine()) {
         if (flops_per_term) *flops_per_term = 8;  // 4 bf16 MACs: (Re, Im) x (hi, lo)
         return fp32_engine() == F32_TC05 ? "dft_tc05_uniform_kernel" : "dft_tc32_uniform_kernel";
+    }
+    if (precision == SHB_FP64 && uniform && tiles == 1 && use_i8_engine()) {
+        if (flops_per_term) *flops_per_term = 32;  // 16 int8 MACs: (Re, Im) x 8 digits
+        return "dft_i8_uniform_kernel";
     }
     const bool mma = precision == SHB_FP64 && tiles == 1 && use_mma_engine(uniform != 0, q);
     const bool realf = mma && (uniform || real) && use_real_form();

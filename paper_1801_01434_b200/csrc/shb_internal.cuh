@@ -52,6 +52,12 @@ int tc05_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, 
                      uint64_t c_count, double out_re, double out_im, double *d_out, double *d_prob,
                      double *d_block_sums, uint64_t slot_outputs, cudaStream_t st);
 
+// FP64-accurate uniform-comb DFT on the int8 tensor cores (dft_i8.cu);
+// arguments as shb_dft_uniform, already validated.
+int i8_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin, uint64_t c_count,
+                   double out_re, double out_im, double *d_out, double *d_prob, double *d_block_sums,
+                   uint64_t slot_outputs, cudaStream_t st);
+
 // ------------------------------------------------------------ integer math
 __host__ __device__ inline uint64_t gcd_u64(uint64_t a, uint64_t b)
 {
