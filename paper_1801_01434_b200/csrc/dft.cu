@@ -1000,7 +1000,8 @@ static Fp32Engine fp32_engine()
 static bool use_tc32_engine() { return fp32_engine() != F32_VECTOR; }
 
 // Engine choice for FP64, tiles == 1 (measured, profiles/r01_mma_real.jsonl):
-// * uniform comb and real amplitudes: the real-A DMMA form, 2 real products
+// * uniform comb: the int8 tensor-core engine (use_i8_engine, below);
+// * real amplitudes (and the uniform comb under SHB_DFT_ENGINE=mma): the real-A DMMA form, 2 real products
 //   per phase term (7.7-8.0e12 terms/s at q = 2^24 and 2^30, vs 4.3e12 for the
 //   vector Horner kernel, whose complex recurrence needs 4 FP64 ops per term
 //   whatever the amplitudes);
@@ -1019,12 +1020,14 @@ static bool use_mma_engine(bool uniform, uint64_t q)
     return true;
 }
 
-// FP64-accurate uniform comb on the int8 tensor cores (dft_i8.cu): exact
-// integer products of an 8-digit split of G*2^55.  SHB_DFT_ENGINE=i8.
+// Uniform comb, FP64: the int8 tensor-core engine (dft_i8.cu) by default --
+// exact integer products of an 8-digit split of G*2^55 with FP64 folds, max
+// |dV|/max|V| ~3e-15 against the DMMA engine, 2.14 s vs 9.05 s at q = 2^30
+// (scripts/i8_check.py).  SHB_DFT_ENGINE=mma|vector selects the FP64-pipe kernels.
 static bool use_i8_engine()
 {
     const char *e = getenv("SHB_DFT_ENGINE");
-    return e && e[0] == 'i';
+    return !(e && e[0]) || e[0] == 'i';
 }
 
 static bool use_real_form()

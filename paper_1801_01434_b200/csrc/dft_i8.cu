@@ -27,13 +27,16 @@
 // columns at NB = 64.  The fold over row-blocks (Horner with w^{-BK}), the
 // exact sincospi seeds and the totals are FP64, as in the DMMA engine.
 //
-// Roles (one persistent CTA per SM, 9 warps):
-//  * warp 8, one elected thread: per super-block 2 x 4 x (BK/32) x 2 MMAs
-//    (M = 128 outputs, N = NB row-blocks, K = 32), committed to `full`;
-//  * warps 0-7 (two workers per TMEM lane = output): build the 16 digit
-//    matrices of G for the tile (FP64 phases, exact sincospi every 16 k),
-//    then per super-block load the accumulators (tcgen05.ld 32x32b.x8),
-//    combine the 4 digit pairs to FP64, fold, seed, add to the FP64 total.
+// Roles (one persistent CTA per SM, 4 SPLIT + 1 warps):
+//  * the last warp, one elected thread: per super-block and component
+//    4 x (BK/32) x 2 MMAs (M = 128 outputs, N = NB row-blocks, K = 32) into
+//    that component's half of TMEM, committed to the component's `full`;
+//  * the other warps (SPLIT workers per TMEM lane = output): build the 16
+//    digit matrices of G for the tile (FP64 phases, exact sincospi every 16
+//    k), then per super-block: load the Re accumulators of their row-blocks
+//    (tcgen05.ld 32x32b.x8), combine the digit pairs to FP64, release the Re
+//    half (the MMAs of the next super-block's Re start under the rest), then
+//    the same for Im with the Horner fold, the exact seed and the FP64 total.
 #include <math.h>
 #include <stdlib.h>
 
@@ -50,29 +53,59 @@ constexpr int TILE = 128;  // outputs per tile (MMA M, TMEM lanes)
 #ifndef SHB_I8_BK
 #define SHB_I8_BK 96
 #endif
-#ifndef SHB_I8_ICOMB
-#define SHB_I8_ICOMB 1  // combine digit pairs as int64 before the FP64 conversion
+#ifndef SHB_I8_CONV
+#define SHB_I8_CONV 1  // int64 pair -> FP64: 0 both by I2F (XU pipe), 1 hi by I2F + lo by the
+                       // 1.5*2^52 bit trick (FP64 pipe), 2 both by the bit trick
+#endif
+#ifndef SHB_I8_CHAINS
+#define SHB_I8_CHAINS 1  // interleaved Horner chains in the fold
+#endif
+#ifndef SHB_I8_SEED_EVERY
+#define SHB_I8_SEED_EVERY 16  // exact sincospi seed every this many super-blocks (rotation between)
+#endif
+#ifndef SHB_I8_PHASES
+#define SHB_I8_PHASES 1  // 1: one hand-over per super-block; 2: Re and Im halves handed over separately
+#endif
+#ifndef SHB_I8_SPLIT
+#define SHB_I8_SPLIT 2  // workers per output (TMEM lane)
 #endif
 constexpr int NB = SHB_I8_NB;         // row-blocks per super-block (MMA N)
 constexpr int BK = SHB_I8_BK;         // k per row-block (MMA K total)
 static_assert(BK % 32 == 0 && BK <= 96, "BK: whole K = 32 steps, |D_p| < 2^21");
-static_assert(NB % 16 == 0 && NB >= 16 && NB <= 64, "NB");
+static_assert(NB % 16 == 0 && NB >= 16 && NB <= 64, "NB: 2 x 4 x NB int32 columns <= 512");
 constexpr int NPAIR = 4;              // accumulators per component
 constexpr int NDIG = 8;               // base-128 digits of G * 2^55
 constexpr int KCH = BK / 32;          // MMA K = 32 for 8-bit operands
 constexpr int SB_AMPS = NB * BK;      // amplitudes per super-block
-constexpr int ACC_COLS = 2 * NPAIR * NB;    // TMEM columns of one accumulator buffer
-constexpr int NBUF = 512 / ACC_COLS;        // 1 at NB = 64, 2 at NB = 32
+constexpr int COMP_COLS = NPAIR * NB;       // TMEM columns of one component's accumulators
 constexpr int TMEM_COLS = 512;
 constexpr int A_BYTES = TILE * BK;          // one digit matrix of one component
 constexpr int G_BYTES = 2 * NDIG * A_BYTES; // [comp][digit]
 constexpr int B_BYTES = NB * BK;            // one weight matrix
 constexpr int SMEM_BYTES = G_BYTES + 4 * B_BYTES + 1024;  // G, (128|1) x (ones|mask), alignment slack
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
-constexpr int WORKERS = 256;
+constexpr int SPLIT = SHB_I8_SPLIT;
+constexpr int WORKERS = TILE * SPLIT;
 constexpr int MMA_WARP = WORKERS / 32;
 constexpr int THREADS = WORKERS + 32;
-constexpr int CH = 8;                 // row-blocks per TMEM load burst
+#ifndef SHB_I8_CH
+#define SHB_I8_CH 8
+#endif
+// row-blocks per TMEM load burst (two bursts in flight).  9 warps put 3 on
+// one SMSP, whose 64 KB register file caps every thread at 168 registers.
+constexpr int CH = SHB_I8_CH;
+constexpr int RBW = NB / SPLIT;       // row-blocks per worker in a full super-block
+static_assert(RBW % CH == 0, "whole load bursts per worker");
+constexpr int NCH = RBW / CH;
+constexpr int CHAINS = SHB_I8_CHAINS;
+constexpr int PHASES = SHB_I8_PHASES;
+#ifndef SHB_I8_PREFETCH
+#define SHB_I8_PREFETCH 0  // PHASES == 1: next burst in flight while this one is folded
+#endif
+constexpr bool PREFETCH = SHB_I8_PREFETCH;
+static_assert(CH % CHAINS == 0, "chains interleave within a burst");
+constexpr uint64_t SEED_EVERY = SHB_I8_SEED_EVERY;
+constexpr int LAST_ALIGN = (CH * SPLIT > 16) ? CH * SPLIT : 16;  // last super-block N granule
 constexpr uint32_t LBO = 128;                 // next 16-byte k group
 constexpr uint32_t SBO = (BK / 16) * 128;     // next 8-row group
 
@@ -102,6 +135,15 @@ __device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uin
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+__device__ __forceinline__ bool elect_one()
+{
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
 }
 
 __device__ __forceinline__ void commit(uint64_t *bar)
@@ -134,22 +176,56 @@ __device__ __forceinline__ void ld8(uint32_t taddr, int *v)
                  : "r"(taddr));
 }
 
+__device__ __forceinline__ void ld4(uint32_t taddr, int *v)
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(taddr));
+}
+
+template <int N>
+__device__ __forceinline__ void ldn(uint32_t taddr, int *v)
+{
+    static_assert(N == 4 || N == 8, "burst");
+    if (N == 8)
+        ld8(taddr, v);
+    else
+        ld4(taddr, v);
+}
+
 __device__ __forceinline__ void phase64(uint64_t idx, uint64_t q, double two_over_q, double &c, double &s)
 {
     const int64_t sidx = (idx > (q >> 1)) ? (int64_t)(idx - q) : (int64_t)idx;
     sincospi((double)sidx * two_over_q, &s, &c);
 }
 
+// exact FP64 value of an int64 |x| < 2^51: 1.5*2^52 + x has the same
+// exponent, so the bit pattern is the integer sum (INT pipe) and one DADD
+// removes the bias (FP64 pipe) -- no XU conversion
+__device__ __forceinline__ double i64_to_f64_exact(long long x)
+{
+    return __longlong_as_double(0x4338000000000000LL + x) - 0x1.8p52;
+}
+
 // 2^55 T from the 4 pair accumulators: exact up to the last add
 __device__ __forceinline__ double combine(int d0, int d1, int d2, int d3)
 {
-#if SHB_I8_ICOMB
-    const long long hi = (long long)d0 * 16384 + d1;  // < 2^35, exact
+    const long long hi = (long long)d0 * 16384 + d1;  // |.| < 2^35, exact
     const long long lo = (long long)d2 * 16384 + d3;
+#if SHB_I8_CONV == 3
+    // D_1, D_2, D_3 >= 0 (unsigned digits, non-negative weights): the bias
+    // 1.5*2^52 rides in the high word of the IMAD.WIDE addend
+    (void)hi;
+    (void)lo;
+    const long long hb = (long long)d0 * 16384LL + (long long)(0x4338000000000000ULL | (uint32_t)d1);
+    const unsigned long long lb = (unsigned long long)(uint32_t)d2 * 16384ULL + (0x4338000000000000ULL | (uint32_t)d3);
+    return fma(__longlong_as_double(hb) - 0x1.8p52, 0x1p28, __longlong_as_double((long long)lb) - 0x1.8p52);
+#elif SHB_I8_CONV == 0
     return fma((double)hi, 0x1p28, (double)lo);
+#elif SHB_I8_CONV == 1
+    return fma((double)hi, 0x1p28, i64_to_f64_exact(lo));
 #else
-    const double t = fma(fma((double)d0, 0x1p14, (double)d1), 0x1p14, (double)d2);  // exact (< 2^50)
-    return fma(t, 0x1p14, (double)d3);
+    return fma(i64_to_f64_exact(hi), 0x1p28, i64_to_f64_exact(lo));
 #endif
 }
 
@@ -161,7 +237,19 @@ struct Args {
     double2 *out;
     double *prob;
     double *tile_sums;  // per tile sum of |V|^2 (nullable)
+    unsigned long long *trace;  // SHB_I8_TRACE builds: clock64 stamps of CTA 0 (exploration)
 };
+
+#ifdef SHB_I8_TRACE
+#define I8_TR(cond, slot)                                                                  \
+    do {                                                                                   \
+        if (p.trace && blockIdx.x == 0 && (cond)) p.trace[(slot)] = clock64();             \
+    } while (0)
+#else
+#define I8_TR(cond, slot) \
+    do {                  \
+    } while (0)
+#endif
 
 __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p)
 {
@@ -170,7 +258,8 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;                  // [comp][digit] A operands
     unsigned char *sB = base + G_BYTES;        // [ones128, ones1, mask128, mask1]
-    __shared__ __align__(8) uint64_t full_bar[NBUF], empty_bar[NBUF], a_ready;
+    // per component c: full_bar[c] (MMA -> workers), empty_bar[c] (workers -> MMA)
+    __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2], a_ready;
     __shared__ uint32_t tmem_base_sh;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -178,7 +267,8 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
     const uint64_t nsb = (p.length + SB_AMPS - 1) / SB_AMPS;
     const uint64_t last_amps = p.length - (nsb - 1) * SB_AMPS;  // in (0, SB_AMPS]
     const int last_rb = (int)((last_amps + BK - 1) / BK);
-    const int last_n = ((last_rb + 15) / 16) * 16;  // MMA N multiple of 16; halves of whole 8-column loads
+    // MMA N of the last super-block: a multiple of 16 and of whole load bursts per worker
+    const int last_n = ((last_rb + LAST_ALIGN - 1) / LAST_ALIGN) * LAST_ALIGN;
 
     // weights (B operands: row = row-block jj, K-major, u8): 128 / 1 times ones / last mask
     for (int i = tid; i < NB * BK; i += THREADS) {
@@ -197,9 +287,9 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        for (int b = 0; b < NBUF; b++) {
-            mbar_init(&full_bar[b], 1);
-            mbar_init(&empty_bar[b], WORKERS);
+        for (int c2 = 0; c2 < 2; c2++) {
+            mbar_init(&full_bar[c2], 1);
+            mbar_init(&empty_bar[c2], WORKERS);
         }
         mbar_init(&a_ready, WORKERS);
         fence_mbar_init();
@@ -212,52 +302,65 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
 
     if (warp == MMA_WARP) {
         // ---------------------------------------------------------- MMA issuer
-        if (lane == 0) {
-            const uint32_t aaddr = smem_addr(sA), baddr = smem_addr(sB);
-            uint64_t g = 0;  // super-blocks issued so far (buffer g % NBUF)
-            uint32_t it = 0;
-            for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
-                wait_bar(&a_ready, it & 1u);  // G of this tile is in shared memory
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                for (uint64_t sb = 0; sb < nsb; sb++, g++) {
-                    const uint32_t b = (uint32_t)(g % NBUF);
-                    const uint64_t use = g / NBUF;
-                    if (use >= 1) wait_bar(&empty_bar[b], (uint32_t)(use - 1) & 1u);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const bool last = sb + 1 == nsb;
-                    const int n = last ? last_n : NB;
-                    const uint32_t id_s = idesc(n, true), id_u = idesc(n, false);
-                    const uint32_t w128 = baddr + (last ? 2 : 0) * B_BYTES, w1 = w128 + B_BYTES;
+        // The whole warp walks the loop (barrier waits, uniform descriptor
+        // arithmetic: base descriptor + compile-time offset >> 4); one elected
+        // lane issues.  At N = 64 an int8 MMA is 32 tensor cycles, so the issue
+        // path has to stay short.
+        const uint64_t adesc = smem_desc(smem_addr(sA)), bdesc = smem_desc(smem_addr(sB));
+        uint64_t g = 0;  // super-blocks issued so far
+        uint32_t it = 0;
+        for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
+            wait_bar(&a_ready, it & 1u);  // G of this tile is in shared memory
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            I8_TR(lane == 0 && it < 4, 10000 + it * 1000);
+            for (uint64_t sb = 0; sb < nsb; sb++, g++) {
+                const bool last = sb + 1 == nsb;
+                const int n = last ? last_n : NB;
+                const uint32_t id_s = idesc(n, true), id_u = idesc(n, false);
+                const uint64_t w128 = bdesc + (uint64_t)((last ? 2 : 0) * B_BYTES >> 4), w1 = w128 + (B_BYTES >> 4);
 #pragma unroll
-                    for (int comp = 0; comp < 2; comp++)
+                for (int comp = 0; comp < 2; comp++) {
+                    // this component's accumulators were drained for super-block g - 1
+                    I8_TR(lane == 0 && it < 4 && sb < 100, 10000 + it * 1000 + 1 + 8 * sb + 3 * comp);
+                    if (g >= 1 && (PHASES == 2 || comp == 0)) wait_bar(&empty_bar[comp], (uint32_t)(g - 1) & 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    I8_TR(lane == 0 && it < 4 && sb < 100, 10000 + it * 1000 + 2 + 8 * sb + 3 * comp);
+                    if (elect_one()) {
 #pragma unroll
                         for (int pr = 0; pr < NPAIR; pr++) {
-                            const uint32_t d = tmem + b * ACC_COLS + (comp * NPAIR + pr) * NB;
-                            const uint32_t ahi = aaddr + (comp * NDIG + 2 * pr) * A_BYTES, alo = ahi + A_BYTES;
+                            const uint32_t d = tmem + (comp * NPAIR + pr) * NB;
+                            const uint64_t ahi = adesc + (uint64_t)((comp * NDIG + 2 * pr) * A_BYTES >> 4);
+                            const uint64_t alo = ahi + (A_BYTES >> 4);
 #pragma unroll
                             for (int s = 0; s < KCH; s++) {
-                                const uint32_t koff = s * 2 * LBO;
-                                mma(d, smem_desc(ahi + koff), smem_desc(w128 + koff), pr == 0 ? id_s : id_u, s > 0);
-                                mma(d, smem_desc(alo + koff), smem_desc(w1 + koff), id_u, 1);
+                                const uint64_t koff = (uint64_t)(s * 2 * LBO >> 4);
+                                mma(d, ahi + koff, w128 + koff, pr == 0 ? id_s : id_u, s > 0);
+                                mma(d, alo + koff, w1 + koff, id_u, 1);
                             }
                         }
-                    commit(&full_bar[b]);
+                        if (PHASES == 2 || comp == 1) commit(&full_bar[PHASES == 2 ? comp : 0]);
+                    }
+                    __syncwarp();
+                    I8_TR(lane == 0 && it < 4 && sb < 100, 10000 + it * 1000 + 3 + 8 * sb + 3 * comp);
                 }
             }
         }
-        __syncwarp();
     } else {
         // ------------------------------------- G builders + folders (row = TMEM lane = output)
         // worker w: row = w % 128 (warp w/32 reads TMEM lane quarter (w/32) % 4),
-        // half = w / 128 builds G columns [BK/2 half, BK/2 (half+1)) and folds
-        // row-blocks [n/2 half, n/2 (half+1)) of every super-block
-        const int row = tid & (TILE - 1), half = tid >> 7;
+        // part = w / 128 builds the 16-k groups part, part + SPLIT, ... of G and
+        // folds row-blocks [part n/SPLIT, (part+1) n/SPLIT) of every super-block
+        const int row = tid & (TILE - 1), part = tid >> 7;
         const uint32_t lane_addr = (uint32_t)(32 * (warp & 3)) << 16;
-        __shared__ double vpart[2][TILE];
-        __shared__ double wsum[8];
+        __shared__ double vpart[SPLIT][2][TILE];
+        __shared__ double wsum[WORKERS / 32];
         uint64_t g = 0;
-        for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        uint32_t itw = 0;
+        const bool trw = (tid == 0 || tid == 160);
+        const int trb = tid == 0 ? 0 : 5000;
+        for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, itw++) {
             const uint64_t c = p.c_begin + t * TILE + row;
+            I8_TR(trw && itw < 4, trb + itw * 1000);
             // G[c, k] = e^{+2 pi i k stride c / q}: exact sincospi every 16 k, FP64
             // rotation in between (<= ~15 ulp, as the DMMA engine's G), rounded to
             // X = rint(G 2^55) and split into 8 digits per component.  The MMAs
@@ -266,7 +369,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
             {
                 double wr, wi;
                 phase64((p.stride * c) & qmask, q, p.two_over_q, wr, wi);
-                for (int k0 = half * (BK / 2); k0 < (half + 1) * (BK / 2); k0 += 16) {
+                for (int k0 = part * 16; k0 < BK; k0 += 16 * SPLIT) {
                     double gr, gi;
                     phase64(((uint64_t)k0 * p.stride * c) & qmask, q, p.two_over_q, gr, gi);
                     uint32_t pk[2][NDIG][4];
@@ -304,63 +407,178 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(&a_ready);
+            I8_TR(trw && itw < 4, trb + itw * 1000 + 1);
 
-            // fold this worker's half of every super-block: h = h * W + 2^55 T[jj] (FP64), W = w^{-BK}
-            double Wr, Wi;
+            // fold this worker's part of every super-block: h = h * W + 2^55 T[jj] (FP64), W = w^{-BK},
+            // as CHAINS interleaved Horner chains with W^CHAINS, joined at the end of the part
+            double Wr, Wi, W2r, W2i, Sr, Si;
             {
                 double co, si;
                 phase64(((uint64_t)BK * p.stride * c) & qmask, q, p.two_over_q, co, si);
                 Wr = co;
                 Wi = -si;
+                phase64(((uint64_t)CHAINS * BK * p.stride * c) & qmask, q, p.two_over_q, co, si);
+                W2r = co;
+                W2i = -si;
+                // seed step between full super-blocks: e^{+2 pi i NB BK stride c / q}
+                phase64(((uint64_t)NB * BK * p.stride * c) & qmask, q, p.two_over_q, Sr, Si);
             }
-            double vr = 0.0, vi = 0.0;
+            double vr = 0.0, vi = 0.0, sdr = 0.0, sdi = 0.0;
             for (uint64_t sb = 0; sb < nsb; sb++, g++) {
-                const uint32_t b = (uint32_t)(g % NBUF);
-                wait_bar(&full_bar[b], (uint32_t)(g / NBUF) & 1u);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const int n = (sb + 1 == nsb) ? last_n : NB;
-                const int j_lo = half * (n / 2), j_hi = j_lo + n / 2;
-                const uint32_t dbase = tmem + lane_addr + b * ACC_COLS;
-                double hr = 0.0, hi = 0.0;
-                for (int j0 = j_lo; j0 < j_hi; j0 += CH) {
-                    int acc[2][NPAIR][CH];
+                const bool last = sb + 1 == nsb;
+                const int n = last ? last_n : NB;
+                const int rbw = n / SPLIT;  // whole load bursts
+                const int j_lo = part * rbw;
+                const uint32_t dre = tmem + lane_addr + j_lo, dim = dre + COMP_COLS;
+                double hr[CHAINS], hi[CHAINS];
 #pragma unroll
-                    for (int comp = 0; comp < 2; comp++)
+                for (int k2 = 0; k2 < CHAINS; k2++) hr[k2] = hi[k2] = 0.0;
+#if SHB_I8_PHASES == 1
+                // one hand-over: per burst both components (Re then Im columns)
+                {
+                    int acc[2][2 * NPAIR][CH];
+                    I8_TR(trw && itw < 4 && sb < 100, trb + itw * 1000 + 2 + 8 * sb);
+                    wait_bar(&full_bar[0], (uint32_t)g & 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    I8_TR(trw && itw < 4 && sb < 100, trb + itw * 1000 + 3 + 8 * sb);
 #pragma unroll
-                        for (int pr = 0; pr < NPAIR; pr++)
-                            ld8(dbase + (comp * NPAIR + pr) * NB + j0, acc[comp][pr]);
+                    for (int pr = 0; pr < 2 * NPAIR; pr++) ldn<CH>(dre + pr * NB, acc[0][pr]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int e = 0; e < CH; e++) {
-                        const double tr = combine(acc[0][0][e], acc[0][1][e], acc[0][2][e], acc[0][3][e]);
-                        const double ti = combine(acc[1][0][e], acc[1][1][e], acc[1][2][e], acc[1][3][e]);
-                        const double nr = fma(hr, Wr, fma(-hi, Wi, tr));
-                        const double ni = fma(hr, Wi, fma(hi, Wr, ti));
-                        hr = nr;
-                        hi = ni;
+                    for (int ch = 0; ch < NCH; ch++) {
+                        if (ch * CH < rbw) {
+                            if (PREFETCH && (ch + 1) * CH < rbw) {
+#pragma unroll
+                                for (int pr = 0; pr < 2 * NPAIR; pr++)
+                                    ldn<CH>(dre + pr * NB + (ch + 1) * CH, acc[(ch + 1) & 1][pr]);
+                            }
+                            const int bi = PREFETCH ? (ch & 1) : 0;
+#pragma unroll
+                            for (int e = 0; e < CH; e++) {
+                                const double tr = combine(acc[bi][0][e], acc[bi][1][e], acc[bi][2][e], acc[bi][3][e]);
+                                const double ti = combine(acc[bi][4][e], acc[bi][5][e], acc[bi][6][e], acc[bi][7][e]);
+                                const int k2 = e % CHAINS;
+                                const double nr = fma(hr[k2], W2r, fma(-hi[k2], W2i, tr));
+                                const double ni = fma(hr[k2], W2i, fma(hi[k2], W2r, ti));
+                                hr[k2] = nr;
+                                hi[k2] = ni;
+                            }
+                            if (!PREFETCH && (ch + 1) * CH < rbw) {
+#pragma unroll
+                                for (int pr = 0; pr < 2 * NPAIR; pr++)
+                                    ldn<CH>(dre + pr * NB + (ch + 1) * CH, acc[0][pr]);
+                            }
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        }
+                    }
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    mbar_arrive(&empty_bar[0]);
+                    I8_TR(trw && itw < 4 && sb < 100, trb + itw * 1000 + 6 + 8 * sb);
+                }
+#else
+                // Re: convert this worker's row-blocks, then hand the Re half back.
+                // Loads run one burst ahead (wait::ld covers the burst issued
+                // before the previous conversions).
+                double tre[RBW];
+                int acc[2][NPAIR][CH];
+                I8_TR(trw && itw < 4 && sb < 100, trb + itw * 1000 + 2 + 8 * sb);
+                wait_bar(&full_bar[0], (uint32_t)g & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                I8_TR(trw && itw < 4 && sb < 100, trb + itw * 1000 + 3 + 8 * sb);
+#pragma unroll
+                for (int pr = 0; pr < NPAIR; pr++) ldn<CH>(dre + pr * NB, acc[0][pr]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int ch = 0; ch < NCH; ch++) {
+                    if (ch * CH < rbw) {
+                        if ((ch + 1) * CH < rbw) {
+#pragma unroll
+                            for (int pr = 0; pr < NPAIR; pr++) ldn<CH>(dre + pr * NB + (ch + 1) * CH, acc[(ch + 1) & 1][pr]);
+                        }
+#pragma unroll
+                        for (int e = 0; e < CH; e++)
+                            tre[ch * CH + e] = combine(acc[ch & 1][0][e], acc[ch & 1][1][e], acc[ch & 1][2][e],
+                                                       acc[ch & 1][3][e]);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(&empty_bar[b]);
-                // seed of the last folded row-block: a0 + (sb*NB + j_hi-1)*BK*stride
-                const uint64_t a_last = p.a0 + ((sb * NB + (uint64_t)(j_hi - 1)) * BK) * p.stride;
+                mbar_arrive(&empty_bar[0]);
+                I8_TR(trw && itw < 4 && sb < 100, trb + itw * 1000 + 4 + 8 * sb);
+                // Im + the Horner over the row-blocks
+                wait_bar(&full_bar[1], (uint32_t)g & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                I8_TR(trw && itw < 4 && sb < 100, trb + itw * 1000 + 5 + 8 * sb);
+#pragma unroll
+                for (int pr = 0; pr < NPAIR; pr++) ldn<CH>(dim + pr * NB, acc[0][pr]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int ch = 0; ch < NCH; ch++) {
+                    if (ch * CH < rbw) {
+                        if ((ch + 1) * CH < rbw) {
+#pragma unroll
+                            for (int pr = 0; pr < NPAIR; pr++) ldn<CH>(dim + pr * NB + (ch + 1) * CH, acc[(ch + 1) & 1][pr]);
+                        }
+#pragma unroll
+                        for (int e = 0; e < CH; e++) {
+                            const double ti = combine(acc[ch & 1][0][e], acc[ch & 1][1][e], acc[ch & 1][2][e],
+                                                      acc[ch & 1][3][e]);
+                            const double tr = tre[ch * CH + e];
+                            const int k2 = e % CHAINS;  // CH % CHAINS == 0: chain of position ch*CH + e
+                            const double nr = fma(hr[k2], W2r, fma(-hi[k2], W2i, tr));
+                            const double ni = fma(hr[k2], W2i, fma(hi[k2], W2r, ti));
+                            hr[k2] = nr;
+                            hi[k2] = ni;
+                        }
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(&empty_bar[1]);
+                I8_TR(trw && itw < 4 && sb < 100, trb + itw * 1000 + 6 + 8 * sb);
+#endif
+                // join the chains: h = (..(h_0 W + h_1) W + ..) W + h_{CHAINS-1}
+                double fr = hr[0], fi = hi[0];
+#pragma unroll
+                for (int k2 = 1; k2 < CHAINS; k2++) {
+                    const double nr = fma(fr, Wr, fma(-fi, Wi, hr[k2]));
+                    const double ni = fma(fr, Wi, fma(fi, Wr, hi[k2]));
+                    fr = nr;
+                    fi = ni;
+                }
+                // seed of the last folded row-block, e^{+2 pi i a_last c / q} with
+                // a_last = a0 + (sb*NB + j_lo + rbw - 1)*BK*stride: exact sincospi
+                // for the last super-block and every SEED_EVERY-th, else the
+                // previous seed times S (same full-super-block offset)
                 double sc, ss;
-                phase64((a_last * c) & qmask, q, p.two_over_q, sc, ss);
-                vr = fma(sc, hr, fma(-ss, hi, vr));
-                vi = fma(sc, hi, fma(ss, hr, vi));
+                if (last || sb % SEED_EVERY == 0) {
+                    const uint64_t a_last = p.a0 + ((sb * NB + (uint64_t)(j_lo + rbw - 1)) * BK) * p.stride;
+                    phase64((a_last * c) & qmask, q, p.two_over_q, sc, ss);
+                } else {
+                    sc = fma(sdr, Sr, -sdi * Si);
+                    ss = fma(sdr, Si, sdi * Sr);
+                }
+                sdr = sc;
+                sdi = ss;
+                I8_TR(trw && itw < 4 && sb < 100, trb + itw * 1000 + 7 + 8 * sb);
+                vr = fma(sc, fr, fma(-ss, fi, vr));
+                vi = fma(sc, fi, fma(ss, fr, vi));
             }
-            // combine the two halves (fixed order: half 0 + half 1), then the
+            // combine the parts (fixed order 0, 1, ..., SPLIT-1), then the
             // epilogue: output factor (with 2^-55), |V|^2 (hypot^2, as
             // np.abs(.)**2), tile sum
-            if (half == 1) {
-                vpart[0][row] = vr;
-                vpart[1][row] = vi;
+            if (part > 0) {
+                vpart[part][0][row] = vr;
+                vpart[part][1][row] = vi;
             }
             asm volatile("bar.sync 1, %0;" ::"n"(WORKERS) : "memory");
             double pr = 0.0;
-            if (half == 0) {
-                vr += vpart[0][row];
-                vi += vpart[1][row];
+            if (part == 0) {
+#pragma unroll
+                for (int k2 = 1; k2 < SPLIT; k2++) {
+                    vr += vpart[k2][0][row];
+                    vi += vpart[k2][1][row];
+                }
                 const uint64_t ci = t * TILE + row;
                 if (ci < p.c_count) {
                     const double o_re = vr * p.out_re - vi * p.out_im;
@@ -403,6 +621,14 @@ __global__ void tile_group_sums_kernel(const double *__restrict__ part, uint64_t
 
 }  // namespace i8
 
+#ifdef SHB_I8_TRACE
+static unsigned long long *&i8_trace_ptr()
+{
+    static unsigned long long *p = nullptr;
+    return p;
+}
+#endif
+
 // Caller contract as shb_dft_uniform (validated there); block sums in the
 // caller's shb_dft_num_blocks(c_count, SHB_FP64) layout (slot_outputs per slot).
 int i8_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin, uint64_t c_count,
@@ -429,6 +655,13 @@ int i8_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, ui
         SHB_TRY(scratch_alloc(part, sizeof(double) * a.ntiles, st));
         a.tile_sums = (double *)part.ptr;
     }
+#ifdef SHB_I8_TRACE
+    static unsigned long long *trace_buf = nullptr;
+    if (!trace_buf) SHB_TRY_CUDA(cudaMalloc(&trace_buf, 20000 * sizeof(unsigned long long)));
+    SHB_TRY_CUDA(cudaMemsetAsync(trace_buf, 0, 20000 * sizeof(unsigned long long), st));
+    a.trace = trace_buf;
+    i8_trace_ptr() = trace_buf;
+#endif
     SHB_TRY_CUDA(cudaFuncSetAttribute(dft_i8_uniform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SMEM_BYTES));
     const uint64_t grid = a.ntiles < (uint64_t)sm_count() ? a.ntiles : (uint64_t)sm_count();
@@ -446,3 +679,13 @@ int i8_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, ui
 }
 
 }  // namespace shb
+
+#ifdef SHB_I8_TRACE
+// exploration builds only: copy the 20000 clock64 stamps of the last launch
+extern "C" int shb_i8_trace(unsigned long long *host)
+{
+    cudaDeviceSynchronize();
+    if (!shb::i8_trace_ptr()) return -1;
+    return (int)cudaMemcpy(host, shb::i8_trace_ptr(), 20000 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+}
+#endif

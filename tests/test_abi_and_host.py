@@ -110,9 +110,11 @@ def test_c_abi_demo_compiles_and_links(lib, tmp_path):
 
 def test_dft_engine_choice(lib, monkeypatch):
     """shb_dft_engine names the kernel each DFT entry point launches (no GPU
-    call): real-A DMMA for uniform combs and real amplitudes (4 flops per
-    phase term), complex DMMA otherwise (8), the vector kernel for tiles > 1,
-    the BF16 tensor-core form for the FP32 uniform comb; env overrides."""
+    call): the int8 tensor-core engine for the FP64 uniform comb (16 int8
+    MACs = 32 integer ops per phase term), real-A DMMA for real amplitudes (4
+    flops per phase term), complex DMMA otherwise (8), the vector kernel for
+    tiles > 1, the BF16 tensor-core form for the FP32 uniform comb; env
+    overrides."""
     import ctypes
 
     def eng(uniform, real, q=1 << 30, prec=nat.FP64, tiles=1):
@@ -122,7 +124,7 @@ def test_dft_engine_choice(lib, monkeypatch):
 
     for var in ("SHB_DFT_ENGINE", "SHB_MMA_REAL", "SHB_FP32_ENGINE"):
         monkeypatch.delenv(var, raising=False)
-    assert eng(1, 1) == ("dft_mma_kernel<uniform, real A>", 4)
+    assert eng(1, 1) == ("dft_i8_uniform_kernel", 32)
     assert eng(0, 1) == ("dft_mma_kernel<generic, real A>", 4)
     assert eng(0, 0) == ("dft_mma_kernel<generic, complex A>", 8)
     assert eng(1, 1, tiles=4)[0] == "dft_kernel<uniform>"
@@ -130,6 +132,11 @@ def test_dft_engine_choice(lib, monkeypatch):
     assert eng(0, 1, prec=nat.FP32)[0] == "dft_kernel<generic>"
     # the choice never depends on the output range, only on q and the data
     assert eng(1, 1, q=1 << 8) == eng(1, 1, q=1 << 32)
+    monkeypatch.setenv("SHB_DFT_ENGINE", "i8")
+    assert eng(1, 1) == ("dft_i8_uniform_kernel", 32)
+    assert eng(0, 1) == ("dft_mma_kernel<generic, real A>", 4)
+    monkeypatch.setenv("SHB_DFT_ENGINE", "mma")
+    assert eng(1, 1) == ("dft_mma_kernel<uniform, real A>", 4)
     monkeypatch.setenv("SHB_DFT_ENGINE", "vector")
     assert eng(1, 1) == ("dft_kernel<uniform>", 8)
     monkeypatch.setenv("SHB_DFT_ENGINE", "mma")

@@ -600,13 +600,15 @@ def test_c_abi_demo_program(tmp_path):
     assert "row64 = 8" in r.stdout
 
 
-@pytest.mark.parametrize("engine,real_form", [("vector", "1"), ("mma", "0"), ("mma", "1")])
+@pytest.mark.parametrize("engine,real_form", [("vector", "1"), ("mma", "0"), ("mma", "1"), ("i8", "1")])
 def test_both_fp64_engines_vs_oracle(engine, real_form, monkeypatch):
-    """The FP64 DFT has two kernels for tiles == 1: the vector Horner kernel and
-    the DMMA (FP64 tensor-core) GEMM-factored kernel, the latter in a complex-A
-    and a real-A form (2 DMMAs per k-step; uniform combs and real amplitudes).
-    All against the oracle on ragged sizes, output shards and the uniform /
-    generic / real amplitude paths."""
+    """The FP64 DFT kernels for tiles == 1: the vector Horner kernel, the DMMA
+    (FP64 tensor-core) GEMM-factored kernel in a complex-A and a real-A form
+    (2 DMMAs per k-step; uniform combs and real amplitudes), and the int8
+    tensor-core engine of the uniform comb (8-digit exact split of G, FP64
+    folds; under "i8" the generic/real calls still take DMMA).  All against
+    the oracle on ragged sizes, output shards and the uniform / generic / real
+    amplitude paths."""
     monkeypatch.setenv("SHB_DFT_ENGINE", engine)
     monkeypatch.setenv("SHB_MMA_REAL", real_form)
     rng = np.random.default_rng(21)
@@ -630,6 +632,31 @@ def test_both_fp64_engines_vs_oracle(engine, real_form, monkeypatch):
             refr = oracle.dft_rows(supp, re_h, q, rows)
             assert np.max(np.abs(orl.cpu().numpy().view(np.complex128) - refr)) < 1e-12 * max(1, np.abs(refr).max())
             assert abs(dev.dsum(brl) - float(prl.sum())) <= 1e-9 * float(prl.sum())
+
+
+@pytest.mark.parametrize("M", [6143, 6144, 6145, 2 * 6144 + 97, 3 * 6144 - 1, 40000])
+def test_i8_engine_superblock_edges_vs_oracle(M, monkeypatch):
+    """The int8 tensor-core FP64 engine around its super-block size (64
+    row-blocks x 96 = 6144 amplitudes): full, one-past and ragged last
+    super-blocks (N rounded up to 16 row-blocks, masked weights), against the
+    oracle on sampled rows and on an unaligned output shard, which must also
+    be bitwise identical to the same rows of the full transform."""
+    monkeypatch.setenv("SHB_DFT_ENGINE", "i8")
+    q, c0, r = 1 << 20, 7, 13
+    assert c0 + (M - 1) * r < q
+    rng = np.random.default_rng(M)
+    supp = c0 + r * np.arange(M, dtype=np.uint64)
+    amp = complex(1 / np.sqrt(M))
+    full, pf, bf = dev.dft_uniform(amp, M, c0, r, q, 0, q)
+    rows = np.unique(np.concatenate([rng.integers(0, q, 300, dtype=np.uint64),
+                                     np.array([0, 1, q - 1, q // 2, q // r], dtype=np.uint64)]))
+    ref = oracle.dft_rows(supp, np.full(M, amp), q, rows)
+    got = full.cpu().numpy().view(np.complex128)[rows.astype(np.int64)]
+    assert np.max(np.abs(got - ref)) < 1e-12 * max(1.0, np.abs(ref).max())
+    assert abs(dev.dsum(bf) - 1.0) < 1e-9
+    lo, cnt = 1000, 777
+    sh, _, _ = dev.dft_uniform(amp, M, c0, r, q, lo, cnt)
+    assert torch.equal(sh, full[2 * lo: 2 * (lo + cnt)])
 
 
 def test_dense_dft_selects_real_form_for_real_states():
