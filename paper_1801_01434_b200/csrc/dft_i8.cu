@@ -183,11 +183,22 @@ __device__ __forceinline__ void ld4(uint32_t taddr, int *v)
                  : "r"(taddr));
 }
 
+__device__ __forceinline__ void ld16(uint32_t taddr, int *v)
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+
 template <int N>
 __device__ __forceinline__ void ldn(uint32_t taddr, int *v)
 {
-    static_assert(N == 4 || N == 8, "burst");
-    if (N == 8)
+    static_assert(N == 4 || N == 8 || N == 16, "burst");
+    if (N == 16)
+        ld16(taddr, v);
+    else if (N == 8)
         ld8(taddr, v);
     else
         ld4(taddr, v);
