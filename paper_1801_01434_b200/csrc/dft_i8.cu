@@ -54,8 +54,9 @@ constexpr int TILE = 128;  // outputs per tile (MMA M, TMEM lanes)
 #define SHB_I8_BK 96
 #endif
 #ifndef SHB_I8_CONV
-#define SHB_I8_CONV 1  // int64 pair -> FP64: 0 both by I2F (XU pipe), 1 hi by I2F + lo by the
-                       // 1.5*2^52 bit trick (FP64 pipe), 2 both by the bit trick
+#define SHB_I8_CONV 5  // accumulators -> FP64 (measured, DESIGN 3.1.0): 5 = one IMAD.WIDE bit pattern
+                       // + DADD + one I2F + one DFMA per component; 0-4 = earlier forms (int64 pairs
+                       // by I2F and/or the 1.5*2^52 bit trick; 4 = 2^52 patterns of D_1 and lo)
 #endif
 #ifndef SHB_I8_CHAINS
 #define SHB_I8_CHAINS 1  // interleaved Horner chains in the fold
@@ -98,6 +99,7 @@ constexpr int RBW = NB / SPLIT;       // row-blocks per worker in a full super-b
 static_assert(RBW % CH == 0, "whole load bursts per worker");
 constexpr int NCH = RBW / CH;
 constexpr int CHAINS = SHB_I8_CHAINS;
+constexpr double T_SCALE = SHB_I8_CONV >= 4 ? 0x1p-47 : 0x1p-55;  // units of combine()
 constexpr int PHASES = SHB_I8_PHASES;
 #ifndef SHB_I8_PREFETCH
 #define SHB_I8_PREFETCH 0  // PHASES == 1: next burst in flight while this one is folded
@@ -218,12 +220,35 @@ __device__ __forceinline__ double i64_to_f64_exact(long long x)
     return __longlong_as_double(0x4338000000000000LL + x) - 0x1.8p52;
 }
 
-// 2^55 T from the 4 pair accumulators: exact up to the last add
+// T in units of T_SCALE from the 4 pair accumulators (one final rounding)
 __device__ __forceinline__ double combine(int d0, int d1, int d2, int d3)
 {
     const long long hi = (long long)d0 * 16384 + d1;  // |.| < 2^35, exact
     const long long lo = (long long)d2 * 16384 + d3;
-#if SHB_I8_CONV == 3
+#if SHB_I8_CONV == 5
+    // 2^47 T = D_0 2^34 + H,  H = D_1 2^20 + lo (< 2^42), lo = D_2 2^6 + round(D_3 / 2^8):
+    // one IMAD.WIDE.U32 forms the bit pattern of 2^52 + H (bias in the addend's high
+    // word), one DADD removes it (exact), D_0 (signed) through one I2F, one DFMA
+    (void)hi;
+    (void)lo;
+    const uint32_t l = ((uint32_t)d2 << 6) + (((uint32_t)d3 + 128u) >> 8);
+    unsigned long long hb;
+    asm("{\n\t.reg .b64 a;\n\tmov.b64 a, {%1, %2};\n\tmad.wide.u32 %0, %3, 1048576, a;\n\t}"
+        : "=l"(hb)
+        : "r"(l), "r"(0x43300000u), "r"((uint32_t)d1));
+    return fma((double)d0, 0x1p34, __longlong_as_double((long long)hb) - 0x1p52);
+#elif SHB_I8_CONV == 4
+    // 2^47 T = D_0 2^34 + D_1 2^20 + lo,  lo = D_2 2^6 + round(D_3 / 2^8) (< 2^28, int32):
+    // D_1 and lo enter through the 2^52 bit pattern (exact, FP64 pipe), D_0 (signed)
+    // through one I2F; the 2^-8 rounding of D_3 is <= 2^-48 absolute on T (below the
+    // FP64 rounding of T itself)
+    (void)hi;
+    (void)lo;
+    const uint32_t l = ((uint32_t)d2 << 6) + (((uint32_t)d3 + 128u) >> 8);
+    const double m1 = __hiloint2double(0x43300000, d1) - 0x1p52;
+    const double u = fma(m1, 0x1p20, __hiloint2double(0x43300000, (int)l)) - 0x1p52;  // exact, < 2^42
+    return fma((double)d0, 0x1p34, u);
+#elif SHB_I8_CONV == 3
     // D_1, D_2, D_3 >= 0 (unsigned digits, non-negative weights): the bias
     // 1.5*2^52 rides in the high word of the IMAD.WIDE addend
     (void)hi;
@@ -657,8 +682,8 @@ int i8_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, ui
     a.c_begin = c_begin;
     a.c_count = c_count;
     a.ntiles = (c_count + TILE - 1) / TILE;
-    a.out_re = out_re * 0x1p-55;
-    a.out_im = out_im * 0x1p-55;
+    a.out_re = out_re * T_SCALE;
+    a.out_im = out_im * T_SCALE;
     a.out = (double2 *)d_out;
     a.prob = d_prob;
     Scratch part;
