@@ -105,6 +105,10 @@ constexpr int PHASES = SHB_I8_PHASES;
 #define SHB_I8_PREFETCH 0  // PHASES == 1: next burst in flight while this one is folded
 #endif
 constexpr bool PREFETCH = SHB_I8_PREFETCH;
+#ifndef SHB_I8_BDEDUP
+#define SHB_I8_BDEDUP 0
+#endif
+constexpr bool BDEDUP = SHB_I8_BDEDUP;
 static_assert(CH % CHAINS == 0, "chains interleave within a burst");
 constexpr uint64_t SEED_EVERY = SHB_I8_SEED_EVERY;
 constexpr int LAST_ALIGN = (CH * SPLIT > 16) ? CH * SPLIT : 16;  // last super-block N granule
@@ -225,7 +229,22 @@ __device__ __forceinline__ double combine(int d0, int d1, int d2, int d3)
 {
     const long long hi = (long long)d0 * 16384 + d1;  // |.| < 2^35, exact
     const long long lo = (long long)d2 * 16384 + d3;
-#if SHB_I8_CONV == 5
+#if SHB_I8_CONV == 6
+    // as 5, but D_0 (signed) enters through the 1.5*2^52 bit pattern (one signed
+    // IMAD.WIDE, INT pipe) instead of an I2F (XU pipe): one DFMA gives
+    // D_0 2^34 - 2^52 exactly (|D_0| < 2^21), one DADD adds the 2^52 + H pattern
+    (void)hi;
+    (void)lo;
+    const uint32_t l = ((uint32_t)d2 << 6) + (((uint32_t)d3 + 128u) >> 8);
+    unsigned long long hb;
+    long long b0;
+    asm("{\n\t.reg .b64 a;\n\tmov.b64 a, {%1, %2};\n\tmad.wide.u32 %0, %3, 1048576, a;\n\t}"
+        : "=l"(hb)
+        : "r"(l), "r"(0x43300000u), "r"((uint32_t)d1));
+    asm("mad.wide.s32 %0, %1, 1, %2;" : "=l"(b0) : "r"(d0), "l"(0x4338000000000000LL));
+    const double t0 = fma(__longlong_as_double(b0), 0x1p34, -(0x1.8p86 + 0x1p52));
+    return t0 + __longlong_as_double((long long)hb);
+#elif SHB_I8_CONV == 5
     // 2^47 T = D_0 2^34 + H,  H = D_1 2^20 + lo (< 2^42), lo = D_2 2^6 + round(D_3 / 2^8):
     // one IMAD.WIDE.U32 forms the bit pattern of 2^52 + H (bias in the addend's high
     // word), one DADD removes it (exact), D_0 (signed) through one I2F, one DFMA
@@ -343,6 +362,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
         // lane issues.  At N = 64 an int8 MMA is 32 tensor cycles, so the issue
         // path has to stay short.
         const uint64_t adesc = smem_desc(smem_addr(sA)), bdesc = smem_desc(smem_addr(sB));
+        const uint64_t bdesc_dedup = bdesc & ~((0x3FFFull << 16) | (0x3FFFull << 32));
         uint64_t g = 0;  // super-blocks issued so far
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
@@ -353,7 +373,10 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 const bool last = sb + 1 == nsb;
                 const int n = last ? last_n : NB;
                 const uint32_t id_s = idesc(n, true), id_u = idesc(n, false);
-                const uint64_t w128 = bdesc + (uint64_t)((last ? 2 : 0) * B_BYTES >> 4), w1 = w128 + (B_BYTES >> 4);
+                // SHB_I8_BDEDUP: the all-128 / all-1 weights of a full super-block read
+                // one 8 x 16 B core matrix for every row group and k group (LBO = SBO = 0)
+                const uint64_t bd = (BDEDUP && !last) ? bdesc_dedup : bdesc;
+                const uint64_t w128 = bd + (uint64_t)((last ? 2 : 0) * B_BYTES >> 4), w1 = w128 + (B_BYTES >> 4);
 #pragma unroll
                 for (int comp = 0; comp < 2; comp++) {
                     // this component's accumulators were drained for super-block g - 1
