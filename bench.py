@@ -451,16 +451,25 @@ def _factor_label(outcome) -> str:
     return f" ({'x'.join(str(v) for v in f)})" if f else ""
 
 
+# tcgen05.ld throughput per SM measured on this pool's B200 (scripts/tmem_ld_burst_probe.cu):
+# 8 warps, bursts of 8 x 32x32b.x8 loads 64 columns apart, one wait::ld per burst
+TMEM_LD_BYTES_PER_CLK = 265.7
+
+
 def _i8_roofline(rec, q, M, world, dft_s, sms, clk_mhz, kname, ops_per_term, traffic, traffic_note,
                  fp64_peak_tf, probe_dfma, probe_dmma) -> dict:
     """Roofline of the int8 tensor-core FP64 engine (csrc/dft_i8.cu), per GPU.
 
     Tensor: 16 int8 MACs (32 integer ops) per phase term (Re/Im x 8 digits of
     G*2^55); peak = 2x the measured cuBLAS bf16 rate (kind::i8 dense issues at
-    twice kind::f16 on B200: 4.5 POPS vs 2.25 PFLOPS nominal).  The kernel's
-    measured limiter is the TMEM read path (tcgen05.ld, 64 B/clk/SM): 8 int32
-    accumulators per (output, row-block of 96 terms); that roofline is
-    reported beside it."""
+    twice kind::f16 on B200: 4.5 POPS vs 2.25 PFLOPS nominal).  The kernel
+    alternates the MMA stream (~50 cycles per M128 N64 K32 MMA, ~0.9 of the
+    measured tensor rate) with the workers' drain of the accumulators (issue-
+    bound FP64 conversion + Horner), serialised on the one TMEM accumulator
+    set (clock64 timeline: profiles/r01_i8_timeline_q2_30.txt).  The TMEM read
+    rate (8 int32 accumulators per output and row-block of 96 terms) is
+    reported beside it against the tcgen05.ld rate MEASURED on this B200 for
+    the drain's access pattern (profiles/r01_tmem_ld_probe.txt)."""
     peaks = _measured_peaks()
     bf16 = peaks.get("bf16_tflops")
     peak_tops = 2 * bf16 if bf16 else 4500.0
@@ -472,7 +481,7 @@ def _i8_roofline(rec, q, M, world, dft_s, sms, clk_mhz, kname, ops_per_term, tra
     last_rb = -(-(M - (nsb - 1) * sb_amps) // bk)
     cols = (nsb - 1) * nb + -(-last_rb // 16) * 16
     tmem_bytes = 32 * cols * (q // world)
-    tmem_peak = 64 * sms * clk_mhz * 1e6 / 1e9  # GB/s
+    tmem_peak = TMEM_LD_BYTES_PER_CLK * sms * clk_mhz * 1e6 / 1e9  # GB/s
     return {"bound": "tensor", "achieved": achieved, "peak": peak_tops, "unit": "TOPS",
             "frac": achieved / peak_tops, "traffic": traffic, "traffic_note": traffic_note,
             "traffic_unit": "bytes/launch", "algorithmic_bytes_per_launch": 24 * (q // world),
@@ -482,8 +491,9 @@ def _i8_roofline(rec, q, M, world, dft_s, sms, clk_mhz, kname, ops_per_term, tra
             "int8_ops_per_phase_term": ops_per_term, "ops_per_launch": ops_per_term * terms,
             "tmem_read": {"achieved_gbs": tmem_bytes / dft_s / 1e9, "peak_gbs": tmem_peak,
                           "frac": tmem_bytes / dft_s / 1e9 / tmem_peak, "bytes_per_launch": tmem_bytes,
-                          "peak_source": f"64 B/clk/SM tcgen05.ld (B300_MICROARCH.md TMEM table) x {sms} SMs x "
-                                         f"{clk_mhz:.0f} MHz"},
+                          "peak_source": f"{TMEM_LD_BYTES_PER_CLK:.0f} B/clk/SM tcgen05.ld measured on B200 for the "
+                                         f"drain's pattern (8 warps, bursts of 8 x 32x32b.x8; "
+                                         f"profiles/r01_tmem_ld_probe.txt) x {sms} SMs x {clk_mhz:.0f} MHz"},
             "fp64_equivalent": {"tflops": 4 * terms / dft_s / 1e12, "fp64_peak_tflops": fp64_peak_tf,
                                 "ratio_to_fp64_peak": 4 * terms / dft_s / 1e12 / fp64_peak_tf,
                                 "note": "4 flops per phase term (the real-A FP64 form: amp*cos, amp*sin) against "

@@ -363,6 +363,14 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
         // path has to stay short.
         const uint64_t adesc = smem_desc(smem_addr(sA)), bdesc = smem_desc(smem_addr(sB));
         const uint64_t bdesc_dedup = bdesc & ~((0x3FFFull << 16) | (0x3FFFull << 32));
+#ifdef SHB_I8_ADEDUP_PROBE
+        // timing probe only (WRONG results): every A operand reads one core matrix,
+        // to separate the shared-memory operand reads from the tensor/TMEM cost
+        const uint64_t adesc_probe = adesc & ~((0x3FFFull << 16) | (0x3FFFull << 32));
+#define SHB_I8_ADESC adesc_probe
+#else
+#define SHB_I8_ADESC adesc
+#endif
         uint64_t g = 0;  // super-blocks issued so far
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
@@ -388,7 +396,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
 #pragma unroll
                         for (int pr = 0; pr < NPAIR; pr++) {
                             const uint32_t d = tmem + (comp * NPAIR + pr) * NB;
-                            const uint64_t ahi = adesc + (uint64_t)((comp * NDIG + 2 * pr) * A_BYTES >> 4);
+                            const uint64_t ahi = SHB_I8_ADESC + (uint64_t)((comp * NDIG + 2 * pr) * A_BYTES >> 4);
                             const uint64_t alo = ahi + (A_BYTES >> 4);
 #pragma unroll
                             for (int s = 0; s < KCH; s++) {
@@ -483,6 +491,9 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 phase64(((uint64_t)NB * BK * p.stride * c) & qmask, q, p.two_over_q, Sr, Si);
             }
             double vr = 0.0, vi = 0.0, sdr = 0.0, sdi = 0.0;
+#ifdef SHB_I8_DRAIN_PROBE
+            int probe_x = 0;
+#endif
             for (uint64_t sb = 0; sb < nsb; sb++, g++) {
                 const bool last = sb + 1 == nsb;
                 const int n = last ? last_n : NB;
@@ -512,6 +523,14 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                                     ldn<CH>(dre + pr * NB + (ch + 1) * CH, acc[(ch + 1) & 1][pr]);
                             }
                             const int bi = PREFETCH ? (ch & 1) : 0;
+#ifdef SHB_I8_DRAIN_PROBE
+                            // timing probe only (WRONG results): the loads without the FP64 work
+#pragma unroll
+                            for (int e = 0; e < CH; e++)
+#pragma unroll
+                                for (int pr = 0; pr < 2 * NPAIR; pr++) probe_x ^= acc[bi][pr][e];
+                            if (false)
+#endif
 #pragma unroll
                             for (int e = 0; e < CH; e++) {
                                 const double tr = combine(acc[bi][0][e], acc[bi][1][e], acc[bi][2][e], acc[bi][3][e]);
@@ -623,6 +642,9 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 vr = fma(sc, fr, fma(-ss, fi, vr));
                 vi = fma(sc, fi, fma(ss, fr, vi));
             }
+#ifdef SHB_I8_DRAIN_PROBE
+            vr += (double)probe_x;
+#endif
             // combine the parts (fixed order 0, 1, ..., SPLIT-1), then the
             // epilogue: output factor (with 2^-55), |V|^2 (hypot^2, as
             // np.abs(.)**2), tile sum
