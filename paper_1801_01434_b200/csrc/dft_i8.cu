@@ -111,7 +111,9 @@ constexpr bool PREFETCH = SHB_I8_PREFETCH;
 constexpr bool BDEDUP = SHB_I8_BDEDUP;
 static_assert(CH % CHAINS == 0, "chains interleave within a burst");
 constexpr uint64_t SEED_EVERY = SHB_I8_SEED_EVERY;
-constexpr int LAST_ALIGN = (CH * SPLIT > 16) ? CH * SPLIT : 16;  // last super-block N granule
+constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
+constexpr int LAST_ALIGN = CH * SPLIT / gcd_c(CH * SPLIT, 16) * 16;  // last super-block N granule: lcm(CH SPLIT, 16)
+static_assert(NB % LAST_ALIGN == 0, "the last super-block's N rounds up to at most NB");
 constexpr uint32_t LBO = 128;                 // next 16-byte k group
 constexpr uint32_t SBO = (BK / 16) * 128;     // next 8-row group
 
