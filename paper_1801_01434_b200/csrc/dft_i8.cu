@@ -99,7 +99,7 @@ constexpr int RBW = NB / SPLIT;       // row-blocks per worker in a full super-b
 static_assert(RBW % CH == 0, "whole load bursts per worker");
 constexpr int NCH = RBW / CH;
 constexpr int CHAINS = SHB_I8_CHAINS;
-constexpr double T_SCALE = SHB_I8_CONV >= 4 ? 0x1p-47 : 0x1p-55;  // units of combine()
+constexpr double T_SCALE = (SHB_I8_CONV >= 4 && SHB_I8_CONV <= 6) ? 0x1p-47 : 0x1p-55;  // units of combine()
 constexpr int PHASES = SHB_I8_PHASES;
 #ifndef SHB_I8_PREFETCH
 #define SHB_I8_PREFETCH 0  // PHASES == 1: next burst in flight while this one is folded
@@ -226,12 +226,28 @@ __device__ __forceinline__ double i64_to_f64_exact(long long x)
     return __longlong_as_double(0x4338000000000000LL + x) - 0x1.8p52;
 }
 
+__constant__ uint32_t c_pow2[2] = {1u << 14, 1u << 28};  // CONV 7 multipliers
+
 // T in units of T_SCALE from the 4 pair accumulators (one final rounding)
 __device__ __forceinline__ double combine(int d0, int d1, int d2, int d3)
 {
     const long long hi = (long long)d0 * 16384 + d1;  // |.| < 2^35, exact
     const long long lo = (long long)d2 * 16384 + d3;
-#if SHB_I8_CONV == 6
+#if SHB_I8_CONV == 7
+    // exact at full width: 2^55 T = D_0 2^42 + H',  H' = D_1 2^28 + D_2 2^14 + D_3 < 2^49
+    // (D_1..D_3 >= 0): two IMAD.WIDE.U32 build the bit pattern of 2^52 + H' (bias in the
+    // first addend's high word), one DADD removes it (exact), D_0 through one I2F, one DFMA
+    (void)hi;
+    (void)lo;
+    // (the multipliers come from constant memory so that ptxas keeps one IMAD.WIDE.U32
+    // each instead of expanding a power-of-two multiply into shift/add pairs)
+    unsigned long long t, hb;
+    asm("{\n\t.reg .b64 a;\n\tmov.b64 a, {%1, %2};\n\tmad.wide.u32 %0, %3, %4, a;\n\t}"
+        : "=l"(t)
+        : "r"((uint32_t)d3), "r"(0x43300000u), "r"((uint32_t)d2), "r"(c_pow2[0]));
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(hb) : "r"((uint32_t)d1), "r"(c_pow2[1]), "l"(t));
+    return fma((double)d0, 0x1p42, __longlong_as_double((long long)hb) - 0x1p52);
+#elif SHB_I8_CONV == 6
     // as 5, but D_0 (signed) enters through the 1.5*2^52 bit pattern (one signed
     // IMAD.WIDE, INT pipe) instead of an I2F (XU pipe): one DFMA gives
     // D_0 2^34 - 2^52 exactly (|D_0| < 2^21), one DADD adds the 2^52 + H pattern
