@@ -18,6 +18,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libshorb200.so"
 SOURCES = ["capi.cu", "modexp.cu", "collapse.cu", "dft.cu", "dft_tc05.cu", "dft_i8.cu", "sample.cu", "context.cu"]
+# extra objects: (object stem, source, defines) -- dft_i8.cu once more as the 6-digit engine
+EXTRA = [("dft_i8d6", "dft_i8.cu", ["-DSHB_I8_DIGITS=6"])]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-O2", "-Xptxas", "-v"]
@@ -44,16 +46,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objdir = PKG / "_obj"
     objdir.mkdir(exist_ok=True)
     objs = []
-    for src in SOURCES:
-        obj = objdir / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, "-I", str(PKG.parent / "include"), "-c", str(CSRC / src), "-o", str(obj)]
+    units = [(Path(src).stem, src, []) for src in SOURCES] + EXTRA
+    for stem, src, defs in units:
+        obj = objdir / (stem + ".o")
+        cmd = [nvcc(), *ARCH, *FLAGS, *defs, "-I", str(PKG.parent / "include"), "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(r.stderr)
-        (objdir / (Path(src).stem + ".ptxas.txt")).write_text(r.stderr)
+        (objdir / (stem + ".ptxas.txt")).write_text(r.stderr)
         objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", str(tmp), "-lcudart"]

@@ -42,16 +42,30 @@
 
 #include "shb_internal.cuh"
 
+#ifndef SHB_I8_DIGITS
+#define SHB_I8_DIGITS 8
+#endif
+// build.py compiles this file twice: the FP64-grade 8-digit engine (namespace i8,
+// i8_dft_uniform) and the 6-digit one (namespace i8d6, i8d6_dft_uniform)
+#if SHB_I8_DIGITS == 6
+#define SHB_I8_NS i8d6
+#define SHB_I8_ENTRY i8d6_dft_uniform
+#else
+#define SHB_I8_NS i8
+#define SHB_I8_ENTRY i8_dft_uniform
+#endif
+
 namespace shb {
 
-namespace i8 {
+namespace SHB_I8_NS {
 
 constexpr int TILE = 128;  // outputs per tile (MMA M, TMEM lanes)
+// SHB_I8_DIGITS: base-128 digits of G (8: X = rint(G 2^55), FP64-grade; 6: rint(G 2^41))
 #ifndef SHB_I8_NB
 #define SHB_I8_NB 64
 #endif
 #ifndef SHB_I8_BK
-#define SHB_I8_BK 96
+#define SHB_I8_BK (SHB_I8_DIGITS == 8 ? 96 : 128)
 #endif
 #ifndef SHB_I8_CONV
 #define SHB_I8_CONV 5  // accumulators -> FP64 (measured, DESIGN 3.1.0): 5 = one IMAD.WIDE bit pattern
@@ -72,10 +86,11 @@ constexpr int TILE = 128;  // outputs per tile (MMA M, TMEM lanes)
 #endif
 constexpr int NB = SHB_I8_NB;         // row-blocks per super-block (MMA N)
 constexpr int BK = SHB_I8_BK;         // k per row-block (MMA K total)
-static_assert(BK % 32 == 0 && BK <= 96, "BK: whole K = 32 steps, |D_p| < 2^21");
-static_assert(NB % 16 == 0 && NB >= 16 && NB <= 64, "NB: 2 x 4 x NB int32 columns <= 512");
-constexpr int NPAIR = 4;              // accumulators per component
-constexpr int NDIG = 8;               // base-128 digits of G * 2^55
+constexpr int NDIG = SHB_I8_DIGITS;   // base-128 digits of G * 2^(7 NDIG - 1)
+constexpr int NPAIR = NDIG / 2;       // accumulators per component
+static_assert(NDIG == 8 || NDIG == 6, "digits");
+static_assert(BK % 32 == 0 && BK <= 128, "BK: whole K = 32 steps, |D_p| < 2^21");
+static_assert(NB % 16 == 0 && NB >= 16 && 2 * NPAIR * NB <= 512, "NB: 2 x NPAIR x NB int32 columns <= 512");
 constexpr int KCH = BK / 32;          // MMA K = 32 for 8-bit operands
 constexpr int SB_AMPS = NB * BK;      // amplitudes per super-block
 constexpr int COMP_COLS = NPAIR * NB;       // TMEM columns of one component's accumulators
@@ -83,7 +98,10 @@ constexpr int TMEM_COLS = 512;
 constexpr int A_BYTES = TILE * BK;          // one digit matrix of one component
 constexpr int G_BYTES = 2 * NDIG * A_BYTES; // [comp][digit]
 constexpr int B_BYTES = NB * BK;            // one weight matrix
-constexpr int SMEM_BYTES = G_BYTES + 4 * B_BYTES + 1024;  // G, (128|1) x (ones|mask), alignment slack
+// the all-128 / all-1 weights of full super-blocks: whole matrices, or (6 digits, to
+// fit 12 digit matrices of BK = 128) 1 KB read through the zero-stride descriptor
+constexpr int ONES_BYTES = NDIG == 8 ? B_BYTES : 1024;
+constexpr int SMEM_BYTES = G_BYTES + 2 * ONES_BYTES + 2 * B_BYTES + 1024;  // G, ones x (128|1), mask x (128|1), slack
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 constexpr int SPLIT = SHB_I8_SPLIT;
 constexpr int WORKERS = TILE * SPLIT;
@@ -99,7 +117,8 @@ constexpr int RBW = NB / SPLIT;       // row-blocks per worker in a full super-b
 static_assert(RBW % CH == 0, "whole load bursts per worker");
 constexpr int NCH = RBW / CH;
 constexpr int CHAINS = SHB_I8_CHAINS;
-constexpr double T_SCALE = (SHB_I8_CONV >= 4 && SHB_I8_CONV <= 6) ? 0x1p-47 : 0x1p-55;  // units of combine()
+constexpr double T_SCALE = NDIG == 6 ? 0x1p-41 : (SHB_I8_CONV >= 4 && SHB_I8_CONV <= 6) ? 0x1p-47 : 0x1p-55;  // units of combine()
+static_assert(NDIG == 8 || SHB_I8_PHASES == 1, "6 digits: one hand-over per super-block only");
 constexpr int PHASES = SHB_I8_PHASES;
 #ifndef SHB_I8_PREFETCH
 #define SHB_I8_PREFETCH 0  // PHASES == 1: next burst in flight while this one is folded
@@ -228,6 +247,17 @@ __device__ __forceinline__ double i64_to_f64_exact(long long x)
 
 __constant__ uint32_t c_pow2[2] = {1u << 14, 1u << 28};  // CONV 7 multipliers
 
+// 6 digits: 2^41 T = D_0 2^28 + D_1 2^14 + D_2 (D_1, D_2 >= 0, < 2^21): the 2^52 bit
+// pattern of D_1 2^14 + D_2 (exact), D_0 through one I2F, one DFMA
+__device__ __forceinline__ double combine3(int d0, int d1, int d2)
+{
+    unsigned long long hb;
+    asm("{\n\t.reg .b64 a;\n\tmov.b64 a, {%1, %2};\n\tmad.wide.u32 %0, %3, 16384, a;\n\t}"
+        : "=l"(hb)
+        : "r"((uint32_t)d2), "r"(0x43300000u), "r"((uint32_t)d1));
+    return fma((double)d0, 0x1p28, __longlong_as_double((long long)hb) - 0x1p52);
+}
+
 // T in units of T_SCALE from the 4 pair accumulators (one final rounding)
 __device__ __forceinline__ double combine(int d0, int d1, int d2, int d3)
 {
@@ -348,10 +378,12 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
         const int jj = i / BK, k = i % BK;
         const uint32_t off = kmajor(jj, k);
         const bool live = (uint64_t)jj * BK + k < last_amps;
-        sB[0 * B_BYTES + off] = 128;
-        sB[1 * B_BYTES + off] = 1;
-        sB[2 * B_BYTES + off] = live ? 128 : 0;
-        sB[3 * B_BYTES + off] = live ? 1 : 0;
+        if (off < (uint32_t)ONES_BYTES) {
+            sB[off] = 128;
+            sB[ONES_BYTES + off] = 1;
+        }
+        sB[2 * ONES_BYTES + off] = live ? 128 : 0;
+        sB[2 * ONES_BYTES + B_BYTES + off] = live ? 1 : 0;
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -401,8 +433,9 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 const uint32_t id_s = idesc(n, true), id_u = idesc(n, false);
                 // SHB_I8_BDEDUP: the all-128 / all-1 weights of a full super-block read
                 // one 8 x 16 B core matrix for every row group and k group (LBO = SBO = 0)
-                const uint64_t bd = (BDEDUP && !last) ? bdesc_dedup : bdesc;
-                const uint64_t w128 = bd + (uint64_t)((last ? 2 : 0) * B_BYTES >> 4), w1 = w128 + (B_BYTES >> 4);
+                const uint64_t bd = ((BDEDUP || NDIG != 8) && !last) ? bdesc_dedup : bdesc;
+                const uint64_t w128 = bd + (uint64_t)((last ? 2 * ONES_BYTES : 0) >> 4);
+                const uint64_t w1 = w128 + (uint64_t)((last ? B_BYTES : ONES_BYTES) >> 4);
 #pragma unroll
                 for (int comp = 0; comp < 2; comp++) {
                     // this component's accumulators were drained for super-block g - 1
@@ -462,13 +495,28 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                     for (int e = 0; e < 16; e++) {
 #pragma unroll
                         for (int comp = 0; comp < 2; comp++) {
-                            const long long X = __double2ll_rn((comp ? gi : gr) * 0x1p55);
-                            const int d0 = (int)(X >> 49);
-                            const unsigned long long R = (unsigned long long)(X - ((long long)d0 << 49));
-                            const uint32_t hi28 = (uint32_t)(R >> 21), lo21 = (uint32_t)R & 0x1FFFFFu;
-                            const uint32_t dig[NDIG] = {(uint32_t)d0 & 0xFFu, hi28 >> 21, (hi28 >> 14) & 127u,
-                                                        (hi28 >> 7) & 127u, hi28 & 127u, lo21 >> 14,
-                                                        (lo21 >> 7) & 127u, lo21 & 127u};
+                            uint32_t dig[NDIG];
+                            if constexpr (NDIG == 8) {
+                                const long long X = __double2ll_rn((comp ? gi : gr) * 0x1p55);
+                                const int d0 = (int)(X >> 49);
+                                const unsigned long long R = (unsigned long long)(X - ((long long)d0 << 49));
+                                const uint32_t hi28 = (uint32_t)(R >> 21), lo21 = (uint32_t)R & 0x1FFFFFu;
+                                const uint32_t dd8[8] = {(uint32_t)d0 & 0xFFu, hi28 >> 21, (hi28 >> 14) & 127u,
+                                                         (hi28 >> 7) & 127u, hi28 & 127u, lo21 >> 14,
+                                                         (lo21 >> 7) & 127u, lo21 & 127u};
+#pragma unroll
+                                for (int dd = 0; dd < NDIG; dd++) dig[dd] = dd8[dd % 8];
+                            } else {
+                                // X = rint(G 2^41) = d0 2^35 + u1 2^28 + ... + u5
+                                const long long X = __double2ll_rn((comp ? gi : gr) * 0x1p41);
+                                const int d0 = (int)(X >> 35);
+                                const unsigned long long R = (unsigned long long)(X - ((long long)d0 << 35));
+                                const uint32_t hi21 = (uint32_t)(R >> 14), lo14 = (uint32_t)R & 0x3FFFu;
+                                const uint32_t dd6[6] = {(uint32_t)d0 & 0xFFu, hi21 >> 14, (hi21 >> 7) & 127u,
+                                                         hi21 & 127u, lo14 >> 7, lo14 & 127u};
+#pragma unroll
+                                for (int dd = 0; dd < NDIG; dd++) dig[dd] = dd6[dd % 6];
+                            }
 #pragma unroll
                             for (int dd = 0; dd < NDIG; dd++) {
                                 if ((e & 3) == 0)
@@ -551,8 +599,14 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
 #endif
 #pragma unroll
                             for (int e = 0; e < CH; e++) {
-                                const double tr = combine(acc[bi][0][e], acc[bi][1][e], acc[bi][2][e], acc[bi][3][e]);
-                                const double ti = combine(acc[bi][4][e], acc[bi][5][e], acc[bi][6][e], acc[bi][7][e]);
+                                double tr, ti;
+                                if constexpr (NDIG == 8) {
+                                    tr = combine(acc[bi][0][e], acc[bi][1][e], acc[bi][2][e], acc[bi][3][e]);
+                                    ti = combine(acc[bi][4][e], acc[bi][5][e], acc[bi][6][e], acc[bi][7][e]);
+                                } else {
+                                    tr = combine3(acc[bi][0][e], acc[bi][1][e], acc[bi][2][e]);
+                                    ti = combine3(acc[bi][NPAIR][e], acc[bi][NPAIR + 1][e], acc[bi][NPAIR + 2][e]);
+                                }
                                 const int k2 = e % CHAINS;
                                 const double nr = fma(hr[k2], W2r, fma(-hi[k2], W2i, tr));
                                 const double ni = fma(hr[k2], W2i, fma(hi[k2], W2r, ti));
@@ -718,7 +772,7 @@ __global__ void tile_group_sums_kernel(const double *__restrict__ part, uint64_t
     out[g] = s;
 }
 
-}  // namespace i8
+}  // namespace SHB_I8_NS
 
 #ifdef SHB_I8_TRACE
 static unsigned long long *&i8_trace_ptr()
@@ -730,11 +784,11 @@ static unsigned long long *&i8_trace_ptr()
 
 // Caller contract as shb_dft_uniform (validated there); block sums in the
 // caller's shb_dft_num_blocks(c_count, SHB_FP64) layout (slot_outputs per slot).
-int i8_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin, uint64_t c_count,
+int SHB_I8_ENTRY(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin, uint64_t c_count,
                    double out_re, double out_im, double *d_out, double *d_prob, double *d_block_sums,
                    uint64_t slot_outputs, cudaStream_t st)
 {
-    using namespace i8;
+    using namespace SHB_I8_NS;
     if (length == 0 || c_count == 0) return set_error(SHB_EINVAL, "i8 path needs a non-empty support and output");
     Args a{};
     a.length = length;

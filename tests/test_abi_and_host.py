@@ -135,6 +135,9 @@ def test_dft_engine_choice(lib, monkeypatch):
     monkeypatch.setenv("SHB_DFT_ENGINE", "i8")
     assert eng(1, 1) == ("dft_i8_uniform_kernel", 32)
     assert eng(0, 1) == ("dft_mma_kernel<generic, real A>", 4)
+    monkeypatch.setenv("SHB_DFT_ENGINE", "i8d6")  # opt-in 6-digit split: 12 int8 MACs per term
+    assert eng(1, 1) == ("i8d6::dft_i8_uniform_kernel", 24)
+    assert eng(0, 1) == ("dft_mma_kernel<generic, real A>", 4)
     monkeypatch.setenv("SHB_DFT_ENGINE", "mma")
     assert eng(1, 1) == ("dft_mma_kernel<uniform, real A>", 4)
     monkeypatch.setenv("SHB_DFT_ENGINE", "vector")

@@ -600,7 +600,7 @@ def test_c_abi_demo_program(tmp_path):
     assert "row64 = 8" in r.stdout
 
 
-@pytest.mark.parametrize("engine,real_form", [("vector", "1"), ("mma", "0"), ("mma", "1"), ("i8", "1")])
+@pytest.mark.parametrize("engine,real_form", [("vector", "1"), ("mma", "0"), ("mma", "1"), ("i8", "1"), ("i8d6", "1")])
 def test_both_fp64_engines_vs_oracle(engine, real_form, monkeypatch):
     """The FP64 DFT kernels for tiles == 1: the vector Horner kernel, the DMMA
     (FP64 tensor-core) GEMM-factored kernel in a complex-A and a real-A form
@@ -653,6 +653,34 @@ def test_i8_engine_superblock_edges_vs_oracle(M, monkeypatch):
     ref = oracle.dft_rows(supp, np.full(M, amp), q, rows)
     got = full.cpu().numpy().view(np.complex128)[rows.astype(np.int64)]
     assert np.max(np.abs(got - ref)) < 1e-12 * max(1.0, np.abs(ref).max())
+    assert abs(dev.dsum(bf) - 1.0) < 1e-9
+    lo, cnt = 1000, 777
+    sh, _, _ = dev.dft_uniform(amp, M, c0, r, q, lo, cnt)
+    assert torch.equal(sh, full[2 * lo: 2 * (lo + cnt)])
+
+
+@pytest.mark.parametrize("M", [1, 8191, 8192, 8193, 2 * 8192 + 97, 40000])
+def test_i8_six_digit_engine_vs_oracle(M, monkeypatch):
+    """The opt-in 6-digit int8 engine (SHB_DFT_ENGINE=i8d6: G rounded to
+    2^-41, 3 digit-pair accumulators, super-blocks of 64 x 128 = 8192
+    amplitudes) against the oracle: V within 1e-12 of max|V| (it measures
+    ~1e-13), the probability vector within the north star's FP64 bar
+    (max|dp| <= 1e-9 max p), shards bitwise identical to the full transform."""
+    monkeypatch.setenv("SHB_DFT_ENGINE", "i8d6")
+    q, c0, r = 1 << 20, 5, 11
+    assert c0 + (M - 1) * r < q
+    rng = np.random.default_rng(M + 1)
+    supp = c0 + r * np.arange(M, dtype=np.uint64)
+    amp = complex(1 / np.sqrt(M))
+    full, pf, bf = dev.dft_uniform(amp, M, c0, r, q, 0, q)
+    rows = np.unique(np.concatenate([rng.integers(0, q, 300, dtype=np.uint64),
+                                     np.array([0, 1, q - 1, q // 2, q // r], dtype=np.uint64)]))
+    ref = oracle.dft_rows(supp, np.full(M, amp), q, rows)
+    got = full.cpu().numpy().view(np.complex128)[rows.astype(np.int64)]
+    assert np.max(np.abs(got - ref)) < 1e-12 * max(1.0, np.abs(ref).max())
+    pref = np.abs(ref) ** 2
+    pgot = pf.cpu().numpy()[rows.astype(np.int64)]
+    assert np.max(np.abs(pgot - pref)) <= 1e-9 * max(pref.max(), 1.0 / q)
     assert abs(dev.dsum(bf) - 1.0) < 1e-9
     lo, cnt = 1000, 777
     sh, _, _ = dev.dft_uniform(amp, M, c0, r, q, lo, cnt)
