@@ -1,12 +1,12 @@
 """One launch of the int8 tensor-core FP64 DFT (uniform comb) at q = 2^24, or at
-the bench config q = 2^30 with `big`: ncu target."""
+the bench config q = 2^30 with `big`; `d6` selects the 6-digit engine: ncu target."""
 import math
 import os
 import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-os.environ["SHB_DFT_ENGINE"] = "i8"
+os.environ["SHB_DFT_ENGINE"] = "i8d6" if "d6" in sys.argv else "i8"
 
 import torch  # noqa: E402
 
