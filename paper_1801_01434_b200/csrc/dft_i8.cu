@@ -68,9 +68,9 @@ constexpr int TILE = 128;  // outputs per tile (MMA M, TMEM lanes)
 #define SHB_I8_BK (SHB_I8_DIGITS == 8 ? 96 : 128)
 #endif
 #ifndef SHB_I8_CONV
-#define SHB_I8_CONV 5  // accumulators -> FP64 (measured, DESIGN 3.1.0): 5 = one IMAD.WIDE bit pattern
-                       // + DADD + one I2F + one DFMA per component; 0-4 = earlier forms (int64 pairs
-                       // by I2F and/or the 1.5*2^52 bit trick; 4 = 2^52 patterns of D_1 and lo)
+#define SHB_I8_CONV 8  // accumulators -> FP64 (measured, DESIGN 3.1.0): 8 = 5 with D_3 truncated (one ALU
+                       // op less); 5 = one IMAD.WIDE bit pattern + DADD + one I2F + one DFMA per
+                       // component; 0-4, 6, 7 = earlier / slower forms
 #endif
 #ifndef SHB_I8_CHAINS
 #define SHB_I8_CHAINS 1  // interleaved Horner chains in the fold
@@ -117,7 +117,7 @@ constexpr int RBW = NB / SPLIT;       // row-blocks per worker in a full super-b
 static_assert(RBW % CH == 0, "whole load bursts per worker");
 constexpr int NCH = RBW / CH;
 constexpr int CHAINS = SHB_I8_CHAINS;
-constexpr double T_SCALE = NDIG == 6 ? 0x1p-41 : (SHB_I8_CONV >= 4 && SHB_I8_CONV <= 6) ? 0x1p-47 : 0x1p-55;  // units of combine()
+constexpr double T_SCALE = NDIG == 6 ? 0x1p-41 : ((SHB_I8_CONV >= 4 && SHB_I8_CONV <= 6) || SHB_I8_CONV == 8) ? 0x1p-47 : 0x1p-55;  // units of combine()
 static_assert(NDIG == 8 || SHB_I8_PHASES == 1, "6 digits: one hand-over per super-block only");
 constexpr int PHASES = SHB_I8_PHASES;
 #ifndef SHB_I8_PREFETCH
@@ -292,6 +292,17 @@ __device__ __forceinline__ double combine(int d0, int d1, int d2, int d3)
     asm("mad.wide.s32 %0, %1, 1, %2;" : "=l"(b0) : "r"(d0), "l"(0x4338000000000000LL));
     const double t0 = fma(__longlong_as_double(b0), 0x1p34, -(0x1.8p86 + 0x1p52));
     return t0 + __longlong_as_double((long long)hb);
+#elif SHB_I8_CONV == 8
+    // as 5 with D_3 / 2^8 truncated instead of rounded (one ALU op less; the
+    // extra 2^-48 absolute on T is below the FP64 rounding of T itself for |T| > 4)
+    (void)hi;
+    (void)lo;
+    const uint32_t l = ((uint32_t)d2 << 6) + ((uint32_t)d3 >> 8);
+    unsigned long long hb;
+    asm("{\n\t.reg .b64 a;\n\tmov.b64 a, {%1, %2};\n\tmad.wide.u32 %0, %3, 1048576, a;\n\t}"
+        : "=l"(hb)
+        : "r"(l), "r"(0x43300000u), "r"((uint32_t)d1));
+    return fma((double)d0, 0x1p34, __longlong_as_double((long long)hb) - 0x1p52);
 #elif SHB_I8_CONV == 5
     // 2^47 T = D_0 2^34 + H,  H = D_1 2^20 + lo (< 2^42), lo = D_2 2^6 + round(D_3 / 2^8):
     // one IMAD.WIDE.U32 forms the bit pattern of 2^52 + H (bias in the addend's high
