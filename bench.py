@@ -524,7 +524,7 @@ def _i8_roofline(rec, q, M, world, dft_s, sms, clk_mhz, kname, ops_per_term, tra
                          "mma_cycles_per_superblock": 2460, "drain_cycles_per_superblock": 2370,
                          "g_build_cycles_per_tile": 7100,
                          "note": "48 MMAs of M128 N64 K32 at ~51 cycles (~0.9 of the measured tensor rate) "
-                                 "alternate with the issue-bound FP64 drain on the one accumulator set"},
+                                 "alternate with the issue- and latency-bound FP64 drain on the one accumulator set"},
             "fp64_equivalent": {"tflops": 4 * terms / dft_s / 1e12, "fp64_peak_tflops": fp64_peak_tf,
                                 "ratio_to_fp64_peak": 4 * terms / dft_s / 1e12 / fp64_peak_tf,
                                 "note": "4 flops per phase term (the real-A FP64 form: amp*cos, amp*sin) against "
