@@ -521,9 +521,9 @@ def _i8_roofline(rec, q, M, world, dft_s, sms, clk_mhz, kname, ops_per_term, tra
                                          f"drain's pattern (8 warps, bursts of 8 x 32x32b.x8; "
                                          f"profiles/r01_tmem_ld_probe.txt) x {sms} SMs x {clk_mhz:.0f} MHz"},
             "timeline": {"source": "profiles/r01_i8_timeline_q2_30.txt (clock64, CTA 0, this config)",
-                         "mma_cycles_per_superblock": 2460, "drain_cycles_per_superblock": 2370,
-                         "g_build_cycles_per_tile": 7100,
-                         "note": "48 MMAs of M128 N64 K32 at ~51 cycles (~0.9 of the measured tensor rate) "
+                         "mma_cycles_per_superblock": 2570, "drain_cycles_per_superblock": 2230,
+                         "g_build_cycles_per_tile": 7200,
+                         "note": "48 MMAs of M128 N64 K32 at ~51-54 cycles (~0.9 of the measured tensor rate) "
                                  "alternate with the issue- and latency-bound FP64 drain on the one accumulator set"},
             "fp64_equivalent": {"tflops": 4 * terms / dft_s / 1e12, "fp64_peak_tflops": fp64_peak_tf,
                                 "ratio_to_fp64_peak": 4 * terms / dft_s / 1e12 / fp64_peak_tf,
