@@ -128,6 +128,10 @@ constexpr bool PREFETCH = SHB_I8_PREFETCH;
 #define SHB_I8_BDEDUP 0
 #endif
 constexpr bool BDEDUP = SHB_I8_BDEDUP;
+#ifndef SHB_I8_GSPLIT
+#define SHB_I8_GSPLIT 0  // 1: build G's Re digits, release them to the MMAs, then Im
+#endif
+constexpr bool GSPLIT = SHB_I8_GSPLIT;
 static_assert(CH % CHAINS == 0, "chains interleave within a burst");
 constexpr uint64_t SEED_EVERY = SHB_I8_SEED_EVERY;
 constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
     unsigned char *sA = base;                  // [comp][digit] A operands
     unsigned char *sB = base + G_BYTES;        // [ones128, ones1, mask128, mask1]
     // per component c: full_bar[c] (MMA -> workers), empty_bar[c] (workers -> MMA)
-    __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2], a_ready;
+    __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2], a_ready[2];
     __shared__ uint32_t tmem_base_sh;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -407,7 +411,8 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
             mbar_init(&full_bar[c2], 1);
             mbar_init(&empty_bar[c2], WORKERS);
         }
-        mbar_init(&a_ready, WORKERS);
+        mbar_init(&a_ready[0], WORKERS);
+        mbar_init(&a_ready[1], WORKERS);
         fence_mbar_init();
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -435,7 +440,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
         uint64_t g = 0;  // super-blocks issued so far
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
-            wait_bar(&a_ready, it & 1u);  // G of this tile is in shared memory
+            wait_bar(&a_ready[0], it & 1u);  // G of this tile (GSPLIT: its Re half) is in shared memory
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             I8_TR(lane == 0 && it < 4, 10000 + it * 1000);
             for (uint64_t sb = 0; sb < nsb; sb++, g++) {
@@ -452,6 +457,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                     // this component's accumulators were drained for super-block g - 1
                     I8_TR(lane == 0 && it < 4 && sb < 100, 10000 + it * 1000 + 1 + 8 * sb + 3 * comp);
                     if (g >= 1 && (PHASES == 2 || comp == 0)) wait_bar(&empty_bar[comp], (uint32_t)(g - 1) & 1u);
+                    if (GSPLIT && comp == 1 && sb == 0) wait_bar(&a_ready[1], it & 1u);  // Im half of G
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     I8_TR(lane == 0 && it < 4 && sb < 100, 10000 + it * 1000 + 2 + 8 * sb + 3 * comp);
                     if (elect_one()) {
@@ -495,7 +501,11 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
             // X = rint(G 2^55) and split into 8 digits per component.  The MMAs
             // reading the previous tile's G are complete: this worker waited on
             // the commit of that tile's last super-block.
-            {
+#pragma unroll
+            for (int cpass = 0; cpass < (GSPLIT ? 2 : 1); cpass++) {
+                // GSPLIT: Re digits first, released to the MMAs (comp 0 of the first
+                // super-block runs under the Im build), then Im
+                const int c_lo = GSPLIT ? cpass : 0, c_hi = GSPLIT ? cpass + 1 : 2;
                 double wr, wi;
                 phase64((p.stride * c) & qmask, q, p.two_over_q, wr, wi);
                 for (int k0 = part * 16; k0 < BK; k0 += 16 * SPLIT) {
@@ -505,7 +515,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
 #pragma unroll
                     for (int e = 0; e < 16; e++) {
 #pragma unroll
-                        for (int comp = 0; comp < 2; comp++) {
+                        for (int comp = c_lo; comp < c_hi; comp++) {
                             uint32_t dig[NDIG];
                             if constexpr (NDIG == 8) {
                                 const long long X = __double2ll_rn((comp ? gi : gr) * 0x1p55);
@@ -542,15 +552,15 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                     }
                     const uint32_t off = kmajor(row, k0);
 #pragma unroll
-                    for (int comp = 0; comp < 2; comp++)
+                    for (int comp = c_lo; comp < c_hi; comp++)
 #pragma unroll
                         for (int dd = 0; dd < NDIG; dd++)
                             *reinterpret_cast<uint4 *>(sA + (comp * NDIG + dd) * A_BYTES + off) =
                                 make_uint4(pk[comp][dd][0], pk[comp][dd][1], pk[comp][dd][2], pk[comp][dd][3]);
                 }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(&a_ready[GSPLIT ? cpass : 0]);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&a_ready);
             I8_TR(trw && itw < 4, trb + itw * 1000 + 1);
 
             // fold this worker's part of every super-block: h = h * W + 2^55 T[jj] (FP64), W = w^{-BK},
