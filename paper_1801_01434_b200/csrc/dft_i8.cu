@@ -132,6 +132,10 @@ constexpr bool BDEDUP = SHB_I8_BDEDUP;
 #define SHB_I8_GSPLIT 0  // 1: build G's Re digits, release them to the MMAs, then Im
 #endif
 constexpr bool GSPLIT = SHB_I8_GSPLIT;
+#ifndef SHB_I8_GPACK
+#define SHB_I8_GPACK 0  // 1: 8-digit G bytes by in-word spreading + PRMT transposes
+#endif
+constexpr bool GPACK = SHB_I8_GPACK;
 static_assert(CH % CHAINS == 0, "chains interleave within a burst");
 constexpr uint64_t SEED_EVERY = SHB_I8_SEED_EVERY;
 constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
@@ -512,6 +516,48 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                     double gr, gi;
                     phase64(((uint64_t)k0 * p.stride * c) & qmask, q, p.two_over_q, gr, gi);
                     uint32_t pk[2][NDIG][4];
+                    if constexpr (GPACK && NDIG == 8) {
+                        // per value: X = rint(G 2^55) = d0 2^49 + R (R = X mod 2^49), digit
+                        // bytes spread within a word (S_hi = u1..u4, S_lo = d0, u5..u7), then a
+                        // 4 x 4 byte transpose (PRMT) across 4 consecutive k per digit
+                        uint32_t sh[2][4], sl[2][4];
+#pragma unroll
+                        for (int e = 0; e < 16; e++) {
+#pragma unroll
+                            for (int comp = c_lo; comp < c_hi; comp++) {
+                                const long long X = __double2ll_rn((comp ? gi : gr) * 0x1p55);
+                                const uint32_t lo = (uint32_t)X, hi = (uint32_t)((unsigned long long)X >> 32);
+                                const uint32_t d0 = (uint32_t)((int)hi >> 17);
+                                const uint32_t h28 = __funnelshift_r(lo, hi & 0x1FFFFu, 21);
+                                sh[comp][e & 3] = (h28 & 0x7Fu) | ((h28 << 1) & 0x7F00u) | ((h28 << 2) & 0x7F0000u) |
+                                                  ((h28 << 3) & 0x7F000000u);
+                                sl[comp][e & 3] = (lo & 0x7Fu) | ((lo << 1) & 0x7F00u) | ((lo << 2) & 0x7F0000u) | (d0 << 24);
+                                if ((e & 3) == 3) {
+                                    const int m = e >> 2;
+                                    // S bytes b0..b3 -> digits: S_hi (4, 3, 2, 1), S_lo (7, 6, 5, 0)
+                                    const uint32_t ah = __byte_perm(sh[comp][0], sh[comp][1], 0x5140),
+                                                   bh = __byte_perm(sh[comp][2], sh[comp][3], 0x5140),
+                                                   ch = __byte_perm(sh[comp][0], sh[comp][1], 0x7362),
+                                                   dh = __byte_perm(sh[comp][2], sh[comp][3], 0x7362);
+                                    pk[comp][4][m] = __byte_perm(ah, bh, 0x5410);
+                                    pk[comp][3][m] = __byte_perm(ah, bh, 0x7632);
+                                    pk[comp][2][m] = __byte_perm(ch, dh, 0x5410);
+                                    pk[comp][1][m] = __byte_perm(ch, dh, 0x7632);
+                                    const uint32_t al = __byte_perm(sl[comp][0], sl[comp][1], 0x5140),
+                                                   bl = __byte_perm(sl[comp][2], sl[comp][3], 0x5140),
+                                                   cl = __byte_perm(sl[comp][0], sl[comp][1], 0x7362),
+                                                   dl = __byte_perm(sl[comp][2], sl[comp][3], 0x7362);
+                                    pk[comp][7][m] = __byte_perm(al, bl, 0x5410);
+                                    pk[comp][6][m] = __byte_perm(al, bl, 0x7632);
+                                    pk[comp][5][m] = __byte_perm(cl, dl, 0x5410);
+                                    pk[comp][0][m] = __byte_perm(cl, dl, 0x7632);
+                                }
+                            }
+                            const double nr = fma(gr, wr, -gi * wi), ni = fma(gr, wi, gi * wr);
+                            gr = nr;
+                            gi = ni;
+                        }
+                    } else {
 #pragma unroll
                     for (int e = 0; e < 16; e++) {
 #pragma unroll
@@ -549,6 +595,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                         const double nr = fma(gr, wr, -gi * wi), ni = fma(gr, wi, gi * wr);
                         gr = nr;
                         gi = ni;
+                    }
                     }
                     const uint32_t off = kmajor(row, k0);
 #pragma unroll
