@@ -136,6 +136,10 @@ constexpr bool GSPLIT = SHB_I8_GSPLIT;
 #define SHB_I8_GPACK 0  // 1: 8-digit G bytes by in-word spreading + PRMT transposes
 #endif
 constexpr bool GPACK = SHB_I8_GPACK;
+#ifndef SHB_I8_MMA_ORDER
+#define SHB_I8_MMA_ORDER 0
+#endif
+constexpr int MMA_ORDER = SHB_I8_MMA_ORDER;
 static_assert(CH % CHAINS == 0, "chains interleave within a burst");
 constexpr uint64_t SEED_EVERY = SHB_I8_SEED_EVERY;
 constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
@@ -466,16 +470,17 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                     I8_TR(lane == 0 && it < 4 && sb < 100, 10000 + it * 1000 + 2 + 8 * sb + 3 * comp);
                     if (elect_one()) {
 #pragma unroll
-                        for (int pr = 0; pr < NPAIR; pr++) {
+                        // MMA_ORDER 0: pair-major (each accumulator's 2 KCH MMAs back to back);
+                        // 1: K-chunk-major (consecutive MMAs rotate over the NPAIR accumulators)
+#pragma unroll
+                        for (int o = 0; o < NPAIR * KCH; o++) {
+                            const int pr = MMA_ORDER ? o % NPAIR : o / KCH, s = MMA_ORDER ? o / NPAIR : o % KCH;
                             const uint32_t d = tmem + (comp * NPAIR + pr) * NB;
                             const uint64_t ahi = SHB_I8_ADESC + (uint64_t)((comp * NDIG + 2 * pr) * A_BYTES >> 4);
                             const uint64_t alo = ahi + (A_BYTES >> 4);
-#pragma unroll
-                            for (int s = 0; s < KCH; s++) {
-                                const uint64_t koff = (uint64_t)(s * 2 * LBO >> 4);
-                                mma(d, ahi + koff, w128 + koff, pr == 0 ? id_s : id_u, s > 0);
-                                mma(d, alo + koff, w1 + koff, id_u, 1);
-                            }
+                            const uint64_t koff = (uint64_t)(s * 2 * LBO >> 4);
+                            mma(d, ahi + koff, w128 + koff, pr == 0 ? id_s : id_u, s > 0);
+                            mma(d, alo + koff, w1 + koff, id_u, 1);
                         }
                         if (PHASES == 2 || comp == 1) commit(&full_bar[PHASES == 2 ? comp : 0]);
                     }
