@@ -3,9 +3,13 @@
 
 One step = one full Shor attempt on the device (modexp -> class counts ->
 collapse -> direct-DFT QFT -> exact Born-rule read), for n = 32399 = 179 x 181,
-q = 2^30, Sampler seed 8 (x = 10594, r = 16020, M = 67025 support elements:
-the attempt factors n through the quantum path).
-Phase terms per step = q * M (outputs x collapsed support).
+q = 2^30, Sampler seed 2 (x = 8477, r = 5340, M = 201075 support elements:
+SURVEY.md 8(d)'s recommended north-star run, which factors n through the
+quantum path in one attempt).  Phase terms per step = q * M (outputs x
+collapsed support).  After the timed steps the line also carries warm
+shor.run_shor factoring times for every BASELINE config (factoring_table),
+the end-to-end C-ABI number with host buffers (e2e) and the CPU port beside
+them.
 
     python bench.py [--gpus N --steps K --warmup W] [--seed 2] [--impl reference]
 
@@ -41,7 +45,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--modulus", dest="n", type=int, default=32399)  # not --n: torchrun prefix-matches it
-    p.add_argument("--seed", type=int, default=8)
+    p.add_argument("--seed", type=int, default=2)
     p.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     p.add_argument("--max-width", type=int, default=32)
     p.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -57,6 +61,7 @@ def parse():
 # ------------------------------------------------------------------ helpers
 
 def workload(n: int, seed: int, max_width: int):
+    """(q, x) of the seeded attempt through the package (the B200 arm)."""
     from paper_1801_01434_b200 import numtheory as nt
     from paper_1801_01434_b200 import qstate, shor
     rw = nt.choose_register_width(n, max_width)
@@ -65,6 +70,18 @@ def workload(n: int, seed: int, max_width: int):
     if math.gcd(x, n) != 1:
         raise SystemExit(f"seed {seed} draws x={x} sharing a factor with n={n}: pick another seed")
     return rw.q, x
+
+
+def bench_config(n: int, seed: int, q: int, x: int, r: int, k: int, c0: int, M: int,
+                 precision: str, world: int) -> dict:
+    """The workload description, identical from both arms (only inputs-derived keys)."""
+    w = q.bit_length() - 1
+    return {"workload": f"n={n} q=2^{w} seed={seed} x={x} r={r} k={k} c0={c0} M={M}: "
+                        f"one full attempt (modexp, collapse, QFT of q*M phase terms, Born read) per step",
+            "n": n, "q": q, "seed": seed, "x": x, "r": r, "k": k, "c0": c0, "M": M,
+            "precision": precision, "parallelism": f"c/a-sharded x{world}",
+            "l2": f"no flush needed: each step writes {24 * q / 2**30:.3g} GiB (spectrum + |V|^2) "
+                  f"{'>>' if 24 * q > 4 * 126e6 else 'vs'} the 126 MB L2"}
 
 
 def cpu_threads() -> int:
@@ -82,31 +99,6 @@ def cpu_model() -> str:
     except OSError:
         pass
     return "unknown"
-
-
-def comb_of(n: int, x: int, q: int, seed: int):
-    """(k, c0, r, M, amp) of the attempt's collapsed register, on the host (exact ints)."""
-    from paper_1801_01434_b200 import numtheory as nt
-    from paper_1801_01434_b200 import qstate
-    r = nt.classical_period(x, n)
-    # class counts: residue x^a for a in [0, q) -> a mod r classes, count_j = floor((q-1-j)/r)+1
-    counts = {}
-    y = 1
-    for j in range(r):
-        counts[y] = (q - 1 - j) // r + 1
-        y = y * x % n
-    import numpy as np
-    carr = np.zeros(n, dtype=np.int64)
-    for v, c in counts.items():
-        carr[v] = c
-    s = qstate.Sampler(seed)
-    s.uniform()  # x draw
-    a_unif = complex(1.0 / math.sqrt(q))
-    w0 = qstate.uniform_weight(a_unif)
-    k = qstate.draw_class(carr, w0, s.uniform())
-    c0 = next(j for j in range(r) if pow(x, j, n) == k)
-    M = (q - 1 - c0) // r + 1
-    return k, c0, r, M, qstate.collapsed_amplitude(a_unif, w0, M)
 
 
 class ClockSampler:
@@ -183,20 +175,25 @@ def cpu_terms_rate(q: int, c0: int, r: int, M: int, amp: complex, seconds: float
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm (oracle port) on the host cores."""
+    """--impl reference: the reference's dense QFT arithmetic on the host cores.
+
+    Imports nothing from paper_1801_01434_b200: the attempt's register comes
+    from oracle.attempt_register (numpy restatement of qstate.py:95-104 and
+    shor.py:67-70) and the rows from oracle/shor_oracle.c, the support-only
+    restatement of _kernels.partial_row_sums (bit-identical to dense_dft)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    q, x = workload(args.n, args.seed, args.max_width)
-    k, c0, r, M, amp = comb_of(args.n, x, q, args.seed)
+    from oracle import oracle
+    reg = oracle.attempt_register(args.n, args.seed)
+    q, x, r, k, c0, M, amp = (reg[key] for key in ("q", "x", "r", "k", "c0", "M", "amp"))
     thr = cpu_threads()
     for _ in range(args.warmup):
         cpu_terms_rate(q, c0, r, M, amp, min(1.0, args.ref_step_seconds), thr)
-    rates, rows, secs = [], 0, 0.0
+    rows, secs = 0, 0.0
     for _ in range(args.steps):
-        rate, nr, el = cpu_terms_rate(q, c0, r, M, amp, args.ref_step_seconds, thr)
-        rates.append(rate)
+        _, nr, el = cpu_terms_rate(q, c0, r, M, amp, args.ref_step_seconds, thr)
         rows += nr
         secs += el
     value = rows * M / secs
@@ -205,10 +202,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (the collapsed register of the seeded attempt)",
-        "config": {"workload": f"n={args.n} q=2^{q.bit_length() - 1} seed={args.seed} x={x} M={M}",
-                   "n": args.n, "q": q, "x": x, "M": M, "precision": "fp64"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if args.precision == "fp64" else "f32",
+        "data": "synthetic (the register is generated by the algorithm from n and the seed)",
+        "config": bench_config(args.n, args.seed, q, x, r, k, c0, M, args.precision, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "port", "sample": sample,
                          "cpu": cpu_model(),
                          "note": "oracle/shor_oracle.c: support-only restatement of "
@@ -367,13 +364,9 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": el_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
         "data": "synthetic (the register is generated by the algorithm from n and the seed)",
-        "config": {"workload": f"n={args.n}{_factor_label(outcome)} q=2^{q.bit_length() - 1} seed={args.seed} "
-                               f"x={x} r={rec.r} M={M}: one full attempt per step",
-                   "n": args.n, "q": q, "x": x, "k": rec.k, "r": rec.r, "M": M, "m": rec.m,
-                   "precision": args.precision, "parallelism": f"c/a-sharded x{world}",
-                   "l2": f"no flush needed: each step writes {24 * q / 2**30:.3g} GiB (spectrum + |V|^2) "
-                         f"{'>>' if 24 * q > 4 * 126e6 else 'vs'} the 126 MB L2",
-                   "outcome": outcome.kind, "factors": list(outcome.factors) if outcome.factors else None},
+        "config": bench_config(args.n, args.seed, q, x, rec.r, rec.k, rec.c0, M, args.precision, world),
+        "result": {"m": rec.m, "outcome": outcome.kind,
+                   "factors": list(outcome.factors) if outcome.factors else None},
         "gpu_launches": int(launches),
         "clocks": clk,
         "roofline": roof,
@@ -386,7 +379,7 @@ def run_b200(args):
     # inside the timed region).  N=1: shb_dense_dft_host (qft.dense_dft); N>1:
     # every rank runs the _kernels.partial_row_sums seam on its row shard.
     if not args.no_e2e:
-        line["e2e"] = e2e_host(args, q, x, lib, torch, nat, rank, world)
+        line["e2e"] = e2e_host(args, q, rec, lib, torch, nat, rank, world)
     # the opt-in 6-digit int8 engine (SHB_DFT_ENGINE=i8d6) on the same attempt: time,
     # m and its probability error against the FP64-grade spectrum just measured
     if not args.no_fp32 and args.precision == "fp64" and "i8" in kname:
@@ -443,28 +436,23 @@ def run_b200(args):
             line["fp32_fast_path"]["bf16_peak_source"] = "MEASURED_PEAKS.json bf16_tflops (cuBLAS, tcgen05)"
 
     if not args.no_factoring:
-        from paper_1801_01434_b200 import qft
         barrier()
-        t0 = time.perf_counter()
         if world == 1:
-            res = shor.run_shor(shor.ShorConfig(n=args.n, seed=args.seed, kernel="dense",
-                                                max_width=args.max_width,
-                                                plan=qft.KernelPlan(precision=args.precision)))
-            ft = time.perf_counter() - t0
-            line["factoring"] = {"api": "shor.run_shor", "time_s": ft, "factors": res.factors,
-                                 "attempts": len(res.attempts),
-                                 "ms": [a.m for a in res.attempts]}
+            line["factoring"] = factoring_table(args)
         else:
             line["factoring"] = {"api": "distributed.sharded_attempt", "time_s": el_ms / args.steps / 1000,
                                  "factors": list(outcome.factors) if outcome.factors else None}
 
     if not args.no_cpu_baseline and world == 1 and rank == 0:
-        k, c0, r, Mh, amp = comb_of(args.n, x, q, args.seed)
+        from oracle import oracle  # the CPU baseline leg: the reference's arithmetic, timed
+        reg = oracle.attempt_register(args.n, args.seed)
         thr = cpu_threads()
-        rate, rows, el = cpu_terms_rate(q, c0, r, Mh, amp, args.cpu_seconds, thr)
+        rate, rows, el = cpu_terms_rate(q, reg["c0"], reg["r"], reg["M"], reg["amp"], args.cpu_seconds, thr)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": thr, "kind": "port",
-                                "sample": f"{rows} random rows x M={Mh} terms of the same attempt in {el:.1f}s",
+                                "sample": f"{rows} random rows x M={reg['M']} terms of the same attempt in {el:.1f}s",
                                 "cpu": cpu_model()}
+        if "factoring" in line:
+            _cpu_column(line["factoring"], args, thr)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -472,9 +460,74 @@ def run_b200(args):
     return 0
 
 
-def _factor_label(outcome) -> str:
-    f = getattr(outcome, "factors", None)
-    return f" ({'x'.join(str(v) for v in f)})" if f else ""
+# BASELINE.json configs through the public driver, with SURVEY.md 8(d)'s traces:
+# (label, n, seed, base_override, expected m per attempt, expected factors)
+FACTORING_CONFIGS = [
+    ("configs[0] n=15 x=7 q=2^8", 15, 0, 7, [64], [3, 5]),
+    ("configs[1] n=221 q=2^16", 221, 0, None, [0, 57344], [13, 17]),
+    ("configs[2] n=3127 q=2^24", 3127, 0, None, [578525], [53, 59]),
+    ("configs[3] n=32399 q=2^30 seed 8 (light)", 32399, 8, None, [342163047], [179, 181]),
+    ("configs[3] n=32399 q=2^30 seed 2 (north-star run)", 32399, 2, None, [874074104], [179, 181]),
+    ("configs[3] n=32399 q=2^30 seed 0 (default seed: odd r, then gcd)", 32399, 0, None, [43968454, None], [179, 181]),
+    ("configs[4] n=46927 q=2^32 seed 0", 46927, 0, None, [175938419, 3920174108], [167, 281]),
+]
+
+
+def factoring_table(args) -> dict:
+    """Warm shor.run_shor (the reference's public driver, shor.py:136-201) for every
+    BASELINE config on this GPU: wall time, per-phase split, QFT phase terms, and
+    the trace checked against SURVEY.md 8(d)."""
+    from paper_1801_01434_b200 import numtheory as nt
+    from paper_1801_01434_b200 import qft, shor
+    rows = []
+    for label, n, seed, base, want_m, want_f in FACTORING_CONFIGS:
+        if n == args.n and (n * n - 1).bit_length() > args.max_width:
+            continue
+        cfg = shor.ShorConfig(n=n, seed=seed, base_override=base, kernel="dense", max_width=32,
+                              plan=qft.KernelPlan(precision=args.precision))
+        t0 = time.perf_counter()
+        res = shor.run_shor(cfg)
+        wall = time.perf_counter() - t0
+        phases = {ph: sum(a.phase_times.get(ph, 0.0) for a in res.attempts) for ph in shor.PHASES}
+        terms = 0
+        for a in res.attempts:
+            if a.k is None:
+                continue
+            r = nt.classical_period(a.x, n)
+            c0 = next(j for j in range(r) if pow(a.x, j, n) == a.k)
+            terms += a.q * ((a.q - 1 - c0) // r + 1)
+        ms = [a.m for a in res.attempts]
+        rows.append({"config": label, "n": n, "seed": seed, "time_s": wall, "factors": res.factors,
+                     "attempts": [{"x": a.x, "k": a.k, "m": a.m, "outcome": a.outcome.kind} for a in res.attempts],
+                     "phase_s": phases, "qft_fraction": phases["qft"] / max(sum(phases.values()), 1e-12),
+                     "phase_terms": terms, "qft_phase_terms_per_s": terms / phases["qft"] if phases["qft"] else None,
+                     "trace_matches_survey": ms == want_m and res.factors == want_f})
+    return {"api": "shor.run_shor(ShorConfig(n, seed, kernel='dense', max_width=32))", "runs": rows,
+            "north_star_time_s": next((r["time_s"] for r in rows if r["n"] == 32399 and r["seed"] == 2), None),
+            "note": "one warm run per config after the timed steps; SURVEY.md 8(d) traces "
+                    "(reference-measured for n <= 3127, closed-form replay of the reference for 2^30 / 2^32)"}
+
+
+def _cpu_column(fact: dict, args, thr: int, seconds: float = 2.0) -> None:
+    """CPU-port QFT estimate beside each factoring row: the oracle rate on a
+    bounded sample of the run's first quantum attempt x its phase terms."""
+    from oracle import oracle
+    for row in fact.get("runs", []):
+        try:
+            reg = oracle.attempt_register(row["n"], row["seed"]) if row["n"] != 15 else None
+        except ValueError:
+            reg = None
+        if row["n"] == 15:
+            q, c0, r, M, amp = 256, 1, 4, 64, complex(0.125)
+        elif reg is None:
+            continue
+        else:
+            q, c0, r, M, amp = reg["q"], reg["c0"], reg["r"], reg["M"], reg["amp"]
+        rate, nrows, el = cpu_terms_rate(q, c0, r, M, amp, seconds, thr)
+        row["cpu_port"] = {"phase_terms_per_s": rate, "cores": thr, "sample_rows": nrows,
+                           "est_qft_s": row["phase_terms"] / rate if row["phase_terms"] else 0.0,
+                           "gpu_speedup": (row["qft_phase_terms_per_s"] / rate
+                                           if row["qft_phase_terms_per_s"] and rate else None)}
 
 
 # tcgen05.ld throughput per SM measured on this pool's B200 (scripts/tmem_ld_burst_probe.cu):
@@ -549,10 +602,15 @@ def ctypes_double():
     return ctypes.c_double(0.0)
 
 
-def e2e_host(args, q, x, lib, torch, nat, rank=0, world=1):
+def e2e_host(args, q, rec, lib, torch, nat, rank=0, world=1, calls=3):
+    """The reference-facing C ABI with HOST buffers: H2D of the complex128[q]
+    register, the DFT and D2H of the spectrum inside each timed call."""
     import ctypes
     import numpy as np
-    k, c0, r, M, amp = comb_of(args.n, x, q, args.seed)
+    from paper_1801_01434_b200 import qstate
+    c0, r, M = rec.c0, rec.r, rec.M
+    a_unif = complex(1.0 / math.sqrt(q))
+    amp = qstate.collapsed_amplitude(a_unif, qstate.uniform_weight(a_unif), M)
     c_lo, c_hi = q * rank // world, q * (rank + 1) // world
     if world > 1:
         shared = _shared_state(q, c0, r, amp, rank, world, torch)
@@ -589,24 +647,39 @@ def e2e_host(args, q, x, lib, torch, nat, rank=0, world=1):
 
     api = ("shb_dense_dft_host (C ABI of qft.dense_dft, pinned host buffers)" if world == 1 else
            "shb_partial_row_sums_host (C ABI of _kernels.partial_row_sums), row shard per rank")
-    # one untimed call at full size: maps the library's stream-ordered pool
-    # (a one-off per process) so the timed call is the steady state
-    call()
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
-    call()
-    el = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([el], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        el = float(t.item())
+    secs = _time_calls(call, calls, world, torch)
     o = out.numpy().view(np.complex128)
     v0 = o[0] if rank == 0 else complex(0)
     del st, out
-    return {"value": q * M / el, "unit": UNIT, "h2d_bytes_per_step": 16 * q * world,
-            "d2h_bytes_per_step": 16 * q, "steps": 1, "warmup": 1, "seconds": el, "api": api,
+    return _e2e_line(q, M, secs, world, api, v0)
+
+
+def _time_calls(call, calls: int, world: int, torch) -> list:
+    """One untimed call (maps the library's stream-ordered pool, a one-off per
+    process), then `calls` timed calls; each is the max over ranks."""
+    call()
+    torch.cuda.synchronize()
+    secs = []
+    for _ in range(calls):
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        call()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            el = float(t.item())
+        secs.append(el)
+    return secs
+
+
+def _e2e_line(q, M, secs, world, api, v0) -> dict:
+    med = statistics.median(secs)
+    return {"value": q * M / med, "unit": UNIT, "h2d_bytes_per_step": 16 * q * world,
+            "d2h_bytes_per_step": 16 * q, "steps": len(secs), "warmup": 1,
+            "seconds": {"median": med, "min": min(secs), "max": max(secs), "all": secs},
+            "value_min_max": [q * M / max(secs), q * M / min(secs)], "api": api,
             "check_V0": [float(v0.real), float(v0.imag)]}
 
 
@@ -654,15 +727,7 @@ def _e2e_sharded(args, q, M, shared, c_lo, c_hi, lib, torch, nat, rank, world):
         nat.check(lib.shb_partial_row_sums_host(ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(shared["ptr"]),
                                                 None, q, c_lo, c_hi, 0, q), "partial_row_sums_host")
 
-    call()  # untimed: maps the pool
-    torch.cuda.synchronize()
-    torch.distributed.barrier()
-    t0 = time.perf_counter()
-    call()
-    el = time.perf_counter() - t0
-    t = torch.tensor([el], dtype=torch.float64, device="cuda")
-    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    el = float(t.item())
+    secs = _time_calls(call, 3, world, torch)
     v0 = out.numpy().view(np.complex128)[0] if rank == 0 else complex(0)
     if shared["registered"]:
         try:
@@ -676,12 +741,10 @@ def _e2e_sharded(args, q, M, shared, c_lo, c_hi, lib, torch, nat, rank, world):
             shared["path"].unlink()
         except OSError:
             pass
-    return {"value": q * M / el, "unit": UNIT, "h2d_bytes_per_step": 16 * q * world,
-            "d2h_bytes_per_step": 16 * q, "steps": 1, "warmup": 1, "seconds": el,
-            "api": "shb_partial_row_sums_host (C ABI of _kernels.partial_row_sums), row shard per rank; "
-                   "one shared /dev/shm host state" + (" page-locked (cudaHostRegister)" if shared["registered"]
-                                                        else " (pageable)"),
-            "check_V0": [float(v0.real), float(v0.imag)]}
+    return _e2e_line(q, M, secs, world,
+                     "shb_partial_row_sums_host (C ABI of _kernels.partial_row_sums), row shard per rank; "
+                     "one shared /dev/shm host state" + (" page-locked (cudaHostRegister)" if shared["registered"]
+                                                          else " (pageable)"), v0)
 
 
 def main():

@@ -206,8 +206,10 @@ int shb_dense_dft_host(const double *state, uint64_t q, uint32_t tiles,
 
 /* _kernels.partial_row_sums(out, state, roots, q, k0, k1, j0, j1)
  * (_kernels.py:16): out[k-k0] = sum_{j0<=j<j1} roots[(j k) mod q] state[j],
- * unscaled.  `roots` is accepted for signature parity and may be NULL: the
- * kernel generates its phases exactly from the integer index. */
+ * unscaled.  `roots` may be NULL; a non-NULL table must be the reference's
+ * e^{+2 pi i j/q} table (spot-checked at six indices, SHB_EINVAL otherwise):
+ * the kernel generates those phases itself from the exact integer index, so
+ * a different table could not be honoured and is rejected, not ignored. */
 int shb_partial_row_sums_host(double *out, const double *state,
                               const double *roots, uint64_t q, uint64_t k0,
                               uint64_t k1, uint64_t j0, uint64_t j1);

@@ -49,6 +49,7 @@ def lib() -> ctypes.CDLL:
         L.oracle_class_counts.argtypes = [vp, u64, u64, vp]
         L.oracle_cumsum_search.argtypes = [vp, u64, f64, vp]
         L.oracle_cumsum_search.restype = u64
+        L.oracle_comb_rows_exact.argtypes = [u64, u64, u64, u64, f64, f64, f64, u64, vp, vp]
         _lib = L
     return _lib
 
@@ -182,6 +183,46 @@ def measure_part2(amplitudes: np.ndarray, residues: np.ndarray, u: float):
     return k, out
 
 
+def attempt_register(n: int, seed: int) -> dict:
+    """The collapsed register of attempt 1 of run_shor(ShorConfig(n, seed=seed)),
+    with the reference's own float64 arithmetic and no q-sized arrays.
+
+    Draw #1 is the base, x = 2 + int(u (n - 3)) (shor.py:67-70); q from
+    numtheory.py:166-175; the residues x^a mod n repeat with period r, so
+    class cycle[j] holds floor((q - 1 - j) / r) + 1 indices (qstate.py:77-82).
+    np.bincount adds each bin's weights sequentially, so a class's probability
+    is the sequential sum of its count copies of |1/sqrt q|^2; the outcome k
+    is the inverse CDF at draw #2 (qstate.py:95-100) and the kept amplitude
+    is amp / sqrt(pairwise sum of the M kept weights) (qstate.py:102-104).
+    Raises ValueError when x shares a factor with n (the gcd shortcut).
+    """
+    w = (n * n - 1).bit_length()
+    q = 1 << w
+    gen = np.random.Generator(np.random.PCG64(int(seed) & 0xFFFFFFFFFFFFFFFF))
+    x = 2 + int(float(gen.random()) * (n - 3))
+    if math.gcd(x, n) != 1:
+        raise ValueError(f"seed {seed}: x={x} shares a factor with n={n}")
+    cycle = [1]
+    v = x % n
+    while v != 1:
+        cycle.append(v)
+        v = v * x % n
+    r = len(cycle)
+    amp0 = np.full(1, 1.0 / math.sqrt(q), dtype=np.complex128)
+    w0 = float(np.abs(amp0[0]) ** 2)
+    counts = np.array([(q - 1 - j) // r + 1 for j in range(r)], dtype=np.int64)
+    seq = {int(c): float(np.cumsum(np.full(int(c), w0))[-1]) for c in np.unique(counts)}
+    ncls = max(cycle) + 1
+    probs = np.zeros(ncls, dtype=np.float64)
+    probs[np.asarray(cycle, dtype=np.int64)] = [seq[int(c)] for c in counts]
+    cum = np.cumsum(probs)
+    k = min(int(np.searchsorted(cum, float(gen.random()) * cum[-1], side="right")), ncls - 1)
+    c0 = cycle.index(k)
+    M = int(counts[c0])
+    amp = complex((amp0 / np.sqrt(np.full(M, w0).sum()))[0])
+    return {"n": n, "q": q, "x": x, "r": r, "k": k, "c0": c0, "M": M, "amp": amp}
+
+
 # ---------------------------------------------------------------- sampling
 
 def probabilities(spectrum: np.ndarray) -> np.ndarray:
@@ -238,4 +279,41 @@ def comb_probabilities(q: int, r: int, c0: int, M: int, rows) -> np.ndarray:
         num = math.sin(math.pi * b_s / q)
         den = math.sin(math.pi * a_s / q)
         out[i] = (num * num) / (q * M * den * den)
+    return out
+
+
+def comb_rows_exact(q: int, r: int, c0: int, M: int, amp: complex, rows, scale: bool = True) -> np.ndarray:
+    """Accuracy reference for a uniform comb's DFT rows (oracle_comb_rows_exact):
+    the geometric-series closed form in long double with exact integer phase
+    reduction, ~1e-18 relative before the final rounding.  Not the reference's
+    arithmetic -- the reference's sequential sum (dft_rows) is the less
+    accurate of the two on peak rows; this says which side of a disagreement
+    is right."""
+    r_ = np.ascontiguousarray(rows, dtype=np.uint64)
+    out = np.empty(2 * r_.size, dtype=np.float64)
+    s = 1.0 / math.sqrt(q) if scale else 1.0
+    lib().oracle_comb_rows_exact(q, r, c0, M, complex(amp).real, complex(amp).imag, s, r_.size, _ptr(r_), _ptr(out))
+    return out.view(np.complex128)
+
+
+def comb_probabilities_vec(q: int, r: int, c0: int, M: int, rows) -> np.ndarray:
+    """comb_probabilities for many rows at once (same arithmetic, numpy).
+
+    Exact integer reduction without overflow for q <= 2^32, r < 2^16, M < 2^20:
+    a = c r mod q < 2^32 from a product < 2^48, then b = a M mod q from a
+    product < 2^52 (c r M mod q = (c r mod q) M mod q).
+    """
+    if q > 1 << 32 or r >= 1 << 16 or M >= 1 << 20:
+        return comb_probabilities(q, r, c0, M, rows)
+    c = np.asarray(rows, dtype=np.uint64)
+    qq, half = np.uint64(q), np.uint64(q // 2)
+    a = (c * np.uint64(r)) % qq
+    b = (a * np.uint64(M)) % qq
+    a_s = np.where(a > half, a.astype(np.float64) - float(q), a.astype(np.float64))
+    b_s = np.where(b > half, b.astype(np.float64) - float(q), b.astype(np.float64))
+    with np.errstate(divide="ignore", invalid="ignore"):
+        num = np.sin(np.pi * (b_s / q))
+        den = np.sin(np.pi * (a_s / q))
+        out = (num * num) / (float(q) * M * den * den)
+    out[a == 0] = M / q
     return out

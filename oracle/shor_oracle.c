@@ -240,3 +240,65 @@ uint64_t oracle_cumsum_search(const double *p, uint64_t L, double u,
     }
     return L - 1; /* searchsorted returns L; the reference clamps to q-1 */
 }
+
+/*
+ * Accuracy reference (not the reference's arithmetic): rows of the DFT of a
+ * uniform comb amp * sum_{j<M} |c0 + j r>, scaled by `scale`, from the
+ * geometric-series closed form in 80-bit long double,
+ *     V_c = amp scale e^{i pi K/q} sin(pi M t/q) / sin(pi t/q),
+ *     t = r c mod q as a signed residue in (-q/2, q/2],
+ *     K = 2 c0 c + (M-1) t mod 2q,
+ * and V_c = amp scale M e^{2 pi i c0 c/q} when t = 0.  Every angle is an
+ * exact integer residue times pi/q, and each sine argument is folded into
+ * [-pi/2, pi/2] (sin(pi - x) = sin x) so a small sine keeps its relative
+ * accuracy; the only errors are long double roundings (~1e-18 relative) and
+ * the final rounding to double.  The reference's own sequential sum
+ * (oracle_dft_rows) carries up to ~M 2^-53 relative error on a peak row;
+ * this function tells which side of a disagreement is the accurate one.
+ */
+static const long double ORACLE_PI_L = 3.141592653589793238462643383279502884L;
+
+/* k mod 2q as a signed residue in (-q, q] */
+static __int128 oracle_mod2q(__int128 k, uint64_t q)
+{
+    const __int128 q2 = 2 * (__int128)q;
+    k %= q2;
+    if (k < 0) k += q2;
+    if (k > (__int128)q) k -= q2;
+    return k;
+}
+
+/* sin(pi k / q) for any integer k, argument folded into [-pi/2, pi/2] */
+static long double oracle_sinpi_over(__int128 k, uint64_t q)
+{
+    k = oracle_mod2q(k, q);
+    const __int128 h = (__int128)(q / 2);
+    if (k > h) k = (__int128)q - k;
+    else if (k < -h) k = -(__int128)q - k;
+    return sinl(ORACLE_PI_L * (long double)k / (long double)q);
+}
+
+void oracle_comb_rows_exact(uint64_t q, uint64_t r, uint64_t c0, uint64_t M,
+                            double amp_re, double amp_im, double scale,
+                            uint64_t nrows, const uint64_t *rows, double *out)
+{
+    for (uint64_t i = 0; i < nrows; i++) {
+        const __int128 c = (__int128)rows[i];
+        __int128 t = (__int128)(((unsigned __int128)r * (unsigned __int128)rows[i]) % q);
+        if (t > (__int128)(q / 2)) t -= (__int128)q;
+        long double mag;
+        __int128 K;
+        if (t == 0) {
+            mag = (long double)M;
+            K = oracle_mod2q(2 * (__int128)c0 * c, q);
+        } else {
+            mag = oracle_sinpi_over((__int128)M * t, q) / oracle_sinpi_over(t, q);
+            K = oracle_mod2q(2 * (__int128)c0 * c + (__int128)(M - 1) * t, q);
+        }
+        const long double ph = ORACLE_PI_L * (long double)K / (long double)q;
+        const long double s = mag * (long double)scale;
+        const long double er = cosl(ph), ei = sinl(ph);
+        out[2 * i] = (double)(s * (er * amp_re - ei * amp_im));
+        out[2 * i + 1] = (double)(s * (er * amp_im + ei * amp_re));
+    }
+}

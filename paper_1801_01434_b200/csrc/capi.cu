@@ -389,15 +389,29 @@ static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t i
                            uint64_t q, uint64_t c_begin, uint64_t c_count, uint32_t tiles,
                            double scale, int precision, double *out_host)
 {
-    cudaStream_t st = nullptr;
+    cudaStream_t st = nullptr, cp = nullptr;
     SHB_TRY_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     struct StreamGuard {
         cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
+        ~StreamGuard() {
+            if (s) cudaStreamDestroy(s);
+        }
     } guard{st};
+    SHB_TRY_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+    StreamGuard cp_guard{cp};
     int rc = SHB_OK;
     {
         Scratch d_state, d_amps, d_out;
+        // declared after the buffers, so destroyed before them on EVERY exit
+        // path: the stream-ordered frees (on st) are enqueued only once both
+        // streams -- including a D2H copy still reading d_out on cp -- drained
+        struct DrainGuard {
+            cudaStream_t a, b;
+            ~DrainGuard() {
+                cudaStreamSynchronize(a);
+                cudaStreamSynchronize(b);
+            }
+        } drain{cp, st};
         SHB_TRY(scratch_alloc(d_state, nstate * 16, st));
         SHB_TRY_CUDA(cudaMemcpyAsync(d_state.ptr, state_host, nstate * 16, cudaMemcpyHostToDevice, st));
         uint64_t a0 = 0, stride = 1, len = 0;
@@ -412,20 +426,19 @@ static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t i
         double ur = 0.0, ui = 0.0;
         if (len) SHB_TRY(shb_progression_kind((const double *)d_amps.ptr, len, &uni, &real, &ur, &ui, st));
         // output slices: slice i's D2H copy (second stream) overlaps slice i+1's
-        // DFT.  Outputs are independent sums, so slicing changes no value.
+        // DFT when out_host is page-locked (pageable memory serialises the copy).
+        // Outputs are independent sums, so slicing changes no value.
         const int nslice = c_count >= (1ull << 22) ? 8 : 1;
-        cudaStream_t cp = nullptr;
-        SHB_TRY_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
-        StreamGuard cp_guard{cp};
         cudaEvent_t ev[8];
-        for (int i = 0; i < nslice; i++) SHB_TRY_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        int nev = 0;
         struct EventGuard {
             cudaEvent_t *e;
-            int n;
+            int *n;
             ~EventGuard() {
-                for (int i = 0; i < n; i++) cudaEventDestroy(e[i]);
+                for (int i = 0; i < *n; i++) cudaEventDestroy(e[i]);
             }
-        } ev_guard{ev, nslice};
+        } ev_guard{ev, &nev};
+        for (; nev < nslice; nev++) SHB_TRY_CUDA(cudaEventCreateWithFlags(&ev[nev], cudaEventDisableTiming));
         double *dout = (double *)d_out.ptr;
         for (int i = 0; i < nslice && rc == SHB_OK; i++) {
             const uint64_t lo = c_count * i / nslice, hi = c_count * (i + 1) / nslice;
@@ -450,6 +463,27 @@ static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t i
     return rc;
 }
 
+/* The reference passes its twiddle table (qft.py:79) to partial_row_sums.
+ * The device derives every phase from the exact integer index instead, which
+ * equals the table up to the table's own rounding; a table that is not
+ * e^{+2 pi i j/q} at all would be silently replaced, so it is rejected.
+ * Spot checks at j = 0, 1, q/8, q/4, q/2, q-1 (5e-15 absolute). */
+static int check_roots_table(const double *roots, uint64_t q)
+{
+    if (!roots) return SHB_OK;
+    const uint64_t idx[6] = {0, 1, q / 8, q / 4, q / 2, q - 1};
+    for (int i = 0; i < 6; i++) {
+        const uint64_t j = idx[i] % q;
+        const double a = (2.0 * M_PI / (double)q) * (double)j;  // qft.py:79's own expression
+        const double cs = cos(a), sn = sin(a);
+        if (fabs(roots[2 * j] - cs) > 5e-15 || fabs(roots[2 * j + 1] - sn) > 5e-15)
+            return set_error(SHB_EINVAL, "roots[%llu] is not e^{+2 pi i j/q}: the device computes the reference "
+                             "twiddle table's values itself and cannot honour a different table",
+                             (unsigned long long)j);
+    }
+    return SHB_OK;
+}
+
 int shb_dense_dft_host(const double *state, uint64_t q, uint32_t tiles, int precision, double *out)
 {
     if (!state || !out) return set_error(SHB_EINVAL, "null buffer");
@@ -462,10 +496,10 @@ int shb_dense_dft_host(const double *state, uint64_t q, uint32_t tiles, int prec
 int shb_partial_row_sums_host(double *out, const double *state, const double *roots, uint64_t q,
                               uint64_t k0, uint64_t k1, uint64_t j0, uint64_t j1)
 {
-    (void)roots;
     if (!state || !out) return set_error(SHB_EINVAL, "null buffer");
     if (q < 2 || (q & (q - 1))) return set_error(SHB_EINVAL, "q must be a power of two >= 2");
     if (k1 < k0 || k1 > q || j1 < j0 || j1 > q) return set_error(SHB_EINVAL, "row/column range outside [0, q)");
+    SHB_TRY(check_roots_table(roots, q));
     if (k1 == k0) return SHB_OK;
     if (j1 == j0) {
         memset(out, 0, (k1 - k0) * 16);

@@ -3,7 +3,7 @@
 Run in the build container only (the reference does not exist on GPU boxes):
 
     NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
-        python tests/golden/make_golden.py
+        python tests/golden/make_golden.py [qreg]
 
 It imports ``shorsim`` from /root/reference/pkg/src (read-only; the numba cache
 is redirected to /tmp so nothing is written into the reference tree) and
@@ -248,7 +248,31 @@ def sampling():
     return {"state": z, "draws": rows}
 
 
+def qreg_dumps():
+    """QREG files written by the reference's own dump path: run_shor with
+    ShorConfig.dump_state_path (shor.py:113-114 -> qstate.dump_state,
+    qstate.py:121-130).  Each attempt overwrites the file, so it holds the
+    last quantum attempt's post-QFT spectrum; stored gzip-compressed."""
+    import gzip
+    import tempfile
+    out = {}
+    for tag, n, kw in [("n15", 15, dict(base_override=7, seed=0)), ("n221", 221, dict(seed=0))]:
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "ref.qreg")
+            r = shor.run_shor(shor.ShorConfig(n=n, kernel="dense", dump_state_path=path, **kw))
+            raw = Path(path).read_bytes()
+        (OUT / f"qreg_{tag}.qreg.gz").write_bytes(gzip.compress(raw, mtime=0))
+        last = [t for t in r.attempts if t.k is not None][-1]
+        out[tag] = {"n": n, "cfg": kw, "factors": r.factors, "bytes": len(raw),
+                    "last_attempt": trace_dict(last)}
+        print(f"  qreg {tag}: {len(raw)} bytes, last attempt x={last.x} m={last.m}", flush=True)
+    (OUT / "qreg_dumps.json").write_text(json.dumps(out, indent=1))
+
+
 def main():
+    if sys.argv[1:] == ["qreg"]:
+        qreg_dumps()
+        return
     t0 = time.time()
     k = kats()
     k["measure_sweep"] = measure_sweep()
@@ -266,6 +290,7 @@ def main():
                         **{f"{key}_{f}": v for key, d in rs.items() for f, v in d.items()})
     smp = sampling()
     np.savez_compressed(OUT / "sampling.npz", state=smp["state"], draws=np.array(smp["draws"]))
+    qreg_dumps()
     print(f"done in {time.time() - t0:.1f}s")
 
 

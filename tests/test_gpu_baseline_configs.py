@@ -1,0 +1,138 @@
+"""GPU parity at BASELINE.json's two largest configs, through the public driver.
+
+``shor.run_shor`` runs n = 32399 at q = 2^30 (Sampler seeds 8, 2, 0) and
+n = 46927 at q = 2^32 (seed 0) end to end on the device.  Every attempt's
+trace (x, k, c0, r, M, m, outcome kind, factors) is asserted against
+SURVEY.md 8(d)'s table (reference: shor.py:136-201, qstate.py:86-114).
+
+Each attempt's QFT output is checked while it is still on the device
+(``qft.transform`` is wrapped, the driver is unchanged):
+
+* every top-r peak row (c = round(j q / r), j < r), the rows around the
+  attempt's m and 2000 random rows against ``oracle.dft_rows`` -- the
+  support-only restatement of ``_kernels.partial_row_sums``, bitwise
+  identical to the reference ``dense_dft``.  The reference
+  sums the M terms sequentially, so on a peak row it carries up to ~M 2^-53
+  of relative rounding error itself (5.9e-12 measured at M = 67025); the
+  bar is therefore max|dV| <= (1e-13 + 2 M 2^-53) max|V| against it, and
+  max|dp| <= 1e-9 max p (north star);
+* the same rows plus 10^6 random rows against ``oracle.comb_rows_exact``,
+  the geometric-series closed form in long double with exact integer phase
+  reduction (~1e-18 relative): bar max|dV| <= 1e-13 max|V|, i.e. the device
+  is FP64-grade where the reference's own sum is not; and the reference
+  rows against it within their 2 M 2^-53 bound (which side is accurate);
+* |V|^2 on the 10^6 random rows against the closed-form probabilities
+  (``oracle.comb_probabilities_vec``): max|dp| <= 1e-9 max p.
+
+About 90 s of GPU time (two 2^32 QFTs dominate) plus ~20 s of oracle rows.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import oracle  # noqa: E402
+from paper_1801_01434_b200 import qft, shor  # noqa: E402
+
+# (x, k, c0, r, M, m, outcome kind) per attempt, then the factors.
+# Attempts that end in the gcd shortcut never reach the register: k/c0/r/M/m are None.
+TRACES = {
+    (32399, 8): ([(10594, 31897, 10943, 16020, 67025, 342163047, "factors")], [179, 181]),
+    (32399, 2): ([(8477, 9557, 4828, 5340, 201075, 874074104, "factors")], [179, 181]),
+    (32399, 0): ([(20637, 8440, 1347, 4005, 268100, 43968454, "retry"),
+                  (537, None, None, None, None, None, "classical_shortcut")], [179, 181]),
+    (46927, 0): ([(29890, 12551, 11799, 23240, 184809, 175938419, "retry"),
+                  (777, 38110, 1363, 11620, 369619, 3920174108, "factors")], [167, 281]),
+}
+
+V_TOL = 1e-13   # max|dV| / max|V| against the accurate closed form
+P_TOL = 1e-9    # max|dp| / max p (north star FP64 bar)
+U = 2.0 ** -53
+
+
+def _check_spectrum(state, spec, m_expected: int, report: dict):
+    """Rows of the device spectrum against the oracles, while it is resident."""
+    q = state.q
+    assert state.full_comb
+    c0, r, M, amp = state.a0, state.stride, state.length, state.amp
+    j = np.arange(r, dtype=np.uint64)
+    peaks = (2 * j * np.uint64(q) + np.uint64(r)) // np.uint64(2 * r) % np.uint64(q)
+    near_m = np.arange(max(0, m_expected - 8), min(q, m_expected + 9), dtype=np.uint64)
+    rng = np.random.default_rng(c0 * 7919 + r)
+    rand = rng.integers(0, q, 2000, dtype=np.uint64)
+    rows = np.unique(np.concatenate([peaks, near_m, rand]))
+
+    def fetch(idx):
+        t = torch.from_numpy(idx.astype(np.int64)).cuda()
+        return spec.data.view(torch.complex128)[t].cpu().numpy(), spec.probabilities()[t].cpu().numpy()
+
+    got, _ = fetch(rows)
+    supp = np.uint64(c0) + np.uint64(r) * np.arange(M, dtype=np.uint64)
+    ref = oracle.dft_rows(supp, np.full(M, amp, dtype=np.complex128), q, rows)
+    exact = oracle.comb_rows_exact(q, r, c0, M, amp, rows)
+    vmax = float(np.abs(exact).max())
+    dv_ref = float(np.abs(got - ref).max()) / vmax
+    dv_exact = float(np.abs(got - exact).max()) / vmax
+    ref_err = float(np.abs(ref - exact).max()) / vmax
+    pref = oracle.probabilities(ref)
+    dp_rows = float(np.abs(oracle.probabilities(got) - pref).max()) / float(pref.max())
+
+    big = rng.integers(0, q, 1_000_000, dtype=np.uint64)
+    vbig, pdev = fetch(big)
+    dv_big = float(np.abs(vbig - oracle.comb_rows_exact(q, r, c0, M, amp, big)).max()) / vmax
+    pcf = oracle.comb_probabilities_vec(q, r, c0, M, big)
+    dp_cf = float(np.abs(pdev - pcf).max()) / max(float(pref.max()), float(pcf.max()))
+
+    report.update(rows=int(rows.size), peaks=int(r), dv_vs_reference=dv_ref, dv_vs_exact=dv_exact,
+                  dv_vs_exact_1e6_rows=dv_big, reference_err_vs_exact=ref_err,
+                  reference_bound=2 * M * U, dp_rows=dp_rows, dp_closed_form=dp_cf)
+    assert dv_exact <= V_TOL and dv_big <= V_TOL, report
+    assert ref_err <= 2 * M * U, report
+    assert dv_ref <= V_TOL + 2 * M * U, report
+    assert dp_rows <= P_TOL, report
+    assert dp_cf <= P_TOL, report
+
+
+def _reference_amplitude(q: int, M: int) -> complex:
+    """amps[sel] / np.sqrt(w[sel].sum()) with numpy's own pairwise sum (qstate.py:95-104)."""
+    a = np.full(1, 1.0 / math.sqrt(q), dtype=np.complex128)
+    w = np.full(M, np.abs(a[0]) ** 2)
+    return complex((a / np.sqrt(w.sum()))[0])
+
+
+@pytest.mark.parametrize("n,seed", [(32399, 8), (32399, 2), (32399, 0), (46927, 0)])
+def test_run_shor_baseline_config(n, seed, monkeypatch):
+    want_attempts, want_factors = TRACES[(n, seed)]
+    quantum = [a for a in want_attempts if a[1] is not None]
+    orig = qft.transform
+    seen = []
+
+    def checked_transform(state, engine, tw=None, plan=None):
+        spec = orig(state, engine, tw, plan)
+        i = len(seen)
+        x, k, c0, r, M, m, _ = quantum[i]
+        report = {"attempt": i, "c0": state.a0, "r": state.stride, "M": state.length}
+        assert (state.a0, state.stride, state.length, state.m) == (c0, r, M, M), report
+        assert state.amp == _reference_amplitude(state.q, M), report
+        _check_spectrum(state, spec, m, report)
+        seen.append(report)
+        return spec
+
+    monkeypatch.setattr(qft, "transform", checked_transform)
+    res = shor.run_shor(shor.ShorConfig(n=n, seed=seed, kernel="dense", max_width=32))
+    assert len(seen) == len(quantum)
+    assert res.succeeded and res.factors == want_factors
+    assert len(res.attempts) == len(want_attempts)
+    for got, (x, k, c0, r, M, m, kind) in zip(res.attempts, want_attempts):
+        assert (got.x, got.k, got.m, got.outcome.kind) == (x, k, m, kind), (n, seed, got)
+        if kind == "factors":
+            assert got.candidate.p % r == 0
+            assert got.q == 1 << (n * n - 1).bit_length()
+    print(f"n={n} seed={seed}:", seen)

@@ -152,3 +152,43 @@ def test_chained_cumsum_reproduces_reference_sampling(golden_dir):
             owner = next(g for g in range(world) if bounds[g][1] > target)
             got = cuts[owner] + oracle.cumsum_search_from(p[cuts[owner]:cuts[owner + 1]], bounds[owner][0], target)
             assert min(got, q - 1) == int(m)
+
+
+@pytest.mark.parametrize("tag,n", [("n221a1", 221), ("n3127", 3127)])
+def test_attempt_register_vs_reference_golden(golden_dir, tag, n):
+    """oracle.attempt_register (the --impl reference arm's register) against the
+    collapse the reference itself produced (attempt 1, seed 0), amplitude bits included."""
+    d = np.load(golden_dir / f"spectrum_{tag}.npz")
+    info = json.loads(str(d["info"]))
+    got = oracle.attempt_register(n, 0)
+    assert (got["q"], got["x"]) == (int(d["q"]), int(d["x"]))
+    assert (got["k"], got["M"], got["c0"], got["r"]) == (info["k"], info["M"], info["c0"], info["r"])
+    assert np.float64(got["amp"].real).view(np.uint64) == np.uint64(int(info["amp_re_bits"], 16))
+    assert got["amp"].imag == 0.0
+
+
+def test_attempt_register_baseline_traces():
+    """SURVEY.md 8(d) attempt-1 registers at q = 2^30 / 2^32 (x, r, k, c0, M)."""
+    want = {(32399, 8): (10594, 16020, 31897, 10943, 67025), (32399, 2): (8477, 5340, 9557, 4828, 201075),
+            (32399, 0): (20637, 4005, 8440, 1347, 268100), (46927, 0): (29890, 23240, 12551, 11799, 184809)}
+    for (n, seed), tr in want.items():
+        g = oracle.attempt_register(n, seed)
+        assert (g["x"], g["r"], g["k"], g["c0"], g["M"]) == tr
+
+
+@pytest.mark.parametrize("tag", ["n15", "n221a1", "n221a2", "n3127"])
+def test_comb_rows_exact_vs_reference_golden(golden_dir, tag):
+    """The long-double closed form (accuracy reference) against the reference's
+    own dense_dft rows: they differ by no more than the reference's sequential
+    rounding bound 2 M 2^-53 max|V|."""
+    d = np.load(golden_dir / f"spectrum_{tag}.npz")
+    info = json.loads(str(d["info"]))
+    if not info.get("comb"):
+        pytest.skip("not a comb")
+    amp = complex(np.uint64(int(info["amp_re_bits"], 16)).view(np.float64),
+                  np.uint64(int(info["amp_im_bits"], 16)).view(np.float64))
+    rows = d["rows"] if "rows" in d.files else np.arange(int(d["q"]))
+    V = d["V"] if "V" in d.files else d["spectrum"]
+    ex = oracle.comb_rows_exact(int(d["q"]), info["r"], info["c0"], info["M"], amp, rows)
+    err = np.abs(ex - V).max() / np.abs(ex).max()
+    assert err <= 2 * info["M"] * 2.0 ** -53, err
