@@ -158,6 +158,24 @@ int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, uint64_t a0,
                     int precision, double *d_out, double *d_prob,
                     double *d_block_sums, void *stream);
 
+/* ------------------------------------------------------ gate-level QFT
+ * The reference's circuit engine primitives (qft.py:164-212) on a device
+ * complex128[q] vector (interleaved re, im), bit-identical to numpy's
+ * arithmetic.  circuit_qft (qft.py:215-231) is built from them in the
+ * Python layer, so the "circuit" engine cross-checks the DFT kernels
+ * independently.  SHB_EINVAL for the reference's argument errors. */
+/* apply_hadamard (qft.py:164-177): (u, v) -> ((u+v)/sqrt2, (u-v)/sqrt2) over
+ * the index pairs differing in bit `qubit`; in place. */
+int shb_apply_hadamard(double *state, uint64_t q, int qubit, void *stream);
+/* apply_controlled_phase (qft.py:180-196): amplitudes whose index has both
+ * bits set are multiplied by (phase_re + i phase_im) = np.exp(1j*angle)
+ * (computed by the caller); in place. */
+int shb_apply_controlled_phase(double *state, uint64_t q, int control, int target,
+                               double phase_re, double phase_im, void *stream);
+/* bit_reverse_permute (qft.py:199-212): out[reverse_bits_w(a)] = in[a];
+ * out of place. */
+int shb_bit_reverse_permute(const double *in, double *out, uint64_t q, void *stream);
+
 /* ---------------------------------------------------------------- sampling
  * qstate.sample_part1 / l2_norm (qstate.py:108-118).
  */

@@ -47,6 +47,9 @@ SIGNATURES = {
     "shb_dft_uniform": ([_f64, _f64, _u64, _u64, _u64, _u64, _u64, _u64, _u32, _f64, _i32, _vp, _vp, _vp, _vp],
                         _i32),
     "shb_dft_num_blocks": ([_u64, _i32], _u64),
+    "shb_apply_hadamard": ([_vp, _u64, _i32, _vp], _i32),
+    "shb_apply_controlled_phase": ([_vp, _u64, _i32, _i32, _f64, _f64, _vp], _i32),
+    "shb_bit_reverse_permute": ([_vp, _vp, _u64, _vp], _i32),
     "shb_probabilities": ([_vp, _u64, _vp, _vp], _i32),
     "shb_sum": ([_vp, _u64, _PF64, _vp], _i32),
     "shb_cumsum_total": ([_vp, _u64, _PF64, _vp], _i32),

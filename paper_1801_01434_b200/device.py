@@ -189,6 +189,25 @@ def dft_uniform(amp: complex, length: int, a0: int, stride: int, q: int, c_begin
     return out, prob, bsum
 
 
+def apply_hadamard(state, q: int, qubit: int) -> None:
+    """In place on a device float64 [2q] vector (qft.py:164-177)."""
+    nat.check(nat.load().shb_apply_hadamard(_vp(state), q, qubit, _stream()), "apply_hadamard")
+
+
+def apply_controlled_phase(state, q: int, control: int, target: int, phase: complex) -> None:
+    """In place; `phase` = np.exp(1j * angle) computed by the caller (qft.py:193)."""
+    nat.check(nat.load().shb_apply_controlled_phase(_vp(state), q, control, target, float(phase.real),
+                                                    float(phase.imag), _stream()), "apply_controlled_phase")
+
+
+def bit_reverse_permute(state, q: int):
+    """Out of place (qft.py:199-212); returns a new device float64 [2q] vector."""
+    t = _t()
+    out = t.empty_like(state)
+    nat.check(nat.load().shb_bit_reverse_permute(_vp(state), _vp(out), q, _stream()), "bit_reverse_permute")
+    return out
+
+
 def probabilities(state):
     t = _t()
     n = state.numel() // 2

@@ -5,9 +5,12 @@ Every engine name maps to ONE implementation, the sm_100a direct-DFT kernel
 (``shb_dft``): it evaluates exactly the sum the reference's ``dense_dft``
 defines, V_k = (1/sqrt q) sum_j e^{+2 pi i jk/q} V_j, over the nonzero
 support only.  ``tiled_dft`` keeps its split-K meaning (input segments summed
-in ascending order).  ``fft_dft`` / ``circuit_qft`` are the same unitary and
-are served by the same kernel (no second backend, no CPU fallback); their
-argument checks are kept.
+in ascending order).  ``fft_dft`` is the same unitary and is served by the
+same kernel (no second backend, no CPU fallback).  ``circuit_qft`` is built
+from the reference's gate primitives (``apply_hadamard``,
+``apply_controlled_phase``, ``bit_reverse_permute``), which run as their own
+device kernels (csrc/gates.cu), so the circuit engine is an independent
+gate-level cross-check of the DFT kernels for w <= 12.
 
 ``block_size`` / ``workers`` of ``KernelPlan`` describe the reference's CPU
 thread decomposition; they are validated as before but do not change the GPU
@@ -185,21 +188,119 @@ def _length(state) -> int:
     return state.q if isinstance(state, dev.DeviceVector) else len(state)
 
 
-def fft_dft(state):
-    """Same transform as qft.py:145-161 (served by the direct-DFT kernel)."""
+def fft_dft(state, precision: str = "fp64"):
+    """Same transform as qft.py:145-161 (served by the direct-DFT kernel).
+
+    `precision` is the plan's (transform passes it): the fast path is
+    honoured here exactly as for the dense engine."""
     q = _length(state)
     _require_power_of_two(q)
-    return _run(state, q, 1, "fp64")
+    if precision not in dev.PRECISIONS:
+        raise ValueError(f"precision must be one of {tuple(dev.PRECISIONS)}")
+    return _run(state, q, 1, precision)
+
+
+# ------------------------------------------------------------- gate level
+# The reference's circuit engine (qft.py:164-231) on device kernels
+# (csrc/gates.cu), bit-identical to its numpy arithmetic.  A numpy input
+# returns numpy; a device vector (register part or spectrum) returns a
+# DeviceSpectrum that stays on the GPU.  Like the reference, every call
+# works on a copy.
+
+def _dense_device_copy(state):
+    """(float64 [2q] device copy of the state, q, came_from_host)."""
+    t = nat.require_cuda()
+    if isinstance(state, dev.DeviceSpectrum):
+        return state.data.clone(), state.q, False
+    if isinstance(state, dev.CollapsedAmplitudes):
+        data = t.zeros(2 * state.q, dtype=t.float64, device="cuda")
+        if state.m:
+            v = data.view(t.complex128)
+            v[state.support] = complex(state.amp)
+        return data, state.q, False
+    if isinstance(state, dev.UniformAmplitudes):
+        data = t.zeros(2 * state.q, dtype=t.float64, device="cuda")
+        data[0::2] = float(state.value)
+        return data, state.q, False
+    arr = np.array(state, dtype=np.complex128)
+    return t.from_numpy(arr.view(np.float64).reshape(-1)).cuda(), arr.size, True
+
+
+def _finish(data, q: int, host: bool):
+    spec = dev.DeviceSpectrum(q, data)
+    return spec.numpy().copy() if host else spec
+
+
+def apply_hadamard(state, qubit_index: int):
+    """qft.py:164-177: (u, v) -> ((u+v)/sqrt2, (u-v)/sqrt2) on bit `qubit_index`."""
+    data, q, host = _dense_device_copy(state)
+    _require_power_of_two(q)
+    w = q.bit_length() - 1
+    if not 0 <= qubit_index < w:
+        raise ValueError(f"qubit index {qubit_index} out of range for w={w}")
+    dev.apply_hadamard(data, q, qubit_index)
+    return _finish(data, q, host)
+
+
+def _phase(angle: float) -> complex:
+    """np.exp(1j * angle) as qft.py:193 evaluates it."""
+    return complex(np.exp(1j * angle))
+
+
+def apply_controlled_phase(state, control: int, target: int, angle: float):
+    """qft.py:180-196: amplitudes with both index bits set times e^{+i angle}."""
+    if control == target:
+        raise ValueError("control and target must differ")
+    data, q, host = _dense_device_copy(state)
+    _require_power_of_two(q)
+    w = q.bit_length() - 1
+    for bit in (control, target):
+        if not 0 <= bit < w:
+            raise ValueError(f"qubit index {bit} out of range for w={w}")
+    dev.apply_controlled_phase(data, q, control, target, _phase(angle))
+    return _finish(data, q, host)
+
+
+def bit_reverse_permute(state):
+    """qft.py:199-212: output[reverse_bits(a)] = input[a] over the full width.
+
+    The reference keeps the input dtype; real and integer inputs are moved
+    as complex128 (exact for |values| < 2^53) and cast back."""
+    if isinstance(state, (dev.DeviceVector,)):
+        data, q, host = _dense_device_copy(state)
+        _require_power_of_two(q)
+        return _finish(dev.bit_reverse_permute(data, q), q, False)
+    a = np.asarray(state)
+    _require_power_of_two(a.size)
+    if a.dtype == np.complex128:
+        return _run_permute(a)
+    if a.dtype.kind == "c":
+        return _run_permute(a.astype(np.complex128)).astype(a.dtype)
+    if a.dtype.kind in "iu" and a.size and int(np.abs(a.astype(object)).max()) >= 1 << 53:
+        raise ValueError("bit_reverse_permute on the device moves values as complex128: "
+                         "integers must be below 2^53 in magnitude")
+    return _run_permute(a.astype(np.complex128)).real.astype(a.dtype)
+
+
+def _run_permute(a: np.ndarray) -> np.ndarray:
+    data, q, _ = _dense_device_copy(a)
+    return _finish(dev.bit_reverse_permute(data, q), q, True)
 
 
 def circuit_qft(state, max_width: int = CIRCUIT_MAX_WIDTH):
-    """Same unitary as the gate-level engine (qft.py:215-231); width cap kept."""
-    q = _length(state)
+    """Gate-level QFT (qft.py:215-231): Hadamards plus controlled phases, then
+    the bit reversal -- O(w^2) device gate launches, width cap kept.  An
+    independent construction of the same unitary as the DFT kernels."""
+    data, q, host = _dense_device_copy(state)
     _require_power_of_two(q)
     w = q.bit_length() - 1
     if w > max_width:
         raise ValueError(f"circuit engine capped at w <= {max_width}, got w={w}")
-    return _run(state, q, 1, "fp64")
+    for i in range(w - 1, -1, -1):
+        dev.apply_hadamard(data, q, i)
+        for j in range(i - 1, -1, -1):
+            dev.apply_controlled_phase(data, q, j, i, _phase(2.0 * np.pi / (1 << (i - j + 1))))
+    return _finish(dev.bit_reverse_permute(data, q), q, host)
 
 
 def transform(state, engine: str, tw: TwiddleTable | None = None, plan: KernelPlan | None = None):
@@ -207,8 +308,11 @@ def transform(state, engine: str, tw: TwiddleTable | None = None, plan: KernelPl
     if engine not in ENGINES:
         raise ValueError(f"unknown engine {engine!r}; expected one of {ENGINES}")
     if engine == "fft":
-        return fft_dft(state)
+        return fft_dft(state, plan.precision if plan is not None else "fp64")
     if engine == "circuit":
+        if plan is not None and plan.precision != "fp64":
+            raise ValueError("the circuit engine is gate-level FP64 only; use dense/tiled/fft for precision="
+                             f"{plan.precision!r}")
         return circuit_qft(state)
     if tw is None:
         tw = build_twiddles(_length(state))

@@ -89,7 +89,7 @@ def entangle_modexp(reg: CompositeRegister, x: int, n: int) -> CompositeRegister
         raise ValueError("register already collapsed")
     if n > 0xFFFFFFFF:
         raise ValueError(f"modulus {n} exceeds the 32-bit residue storage of the B200 path")
-    res = dev.modexp(x, n, reg.q)
+    res = dev.modexp(x % n, n, reg.q)  # the reference walks x % n (qstate.py:78): any int x
     return replace(reg, residues=dev.DeviceResidues(res), n=n, x=x)
 
 

@@ -1,0 +1,211 @@
+// Probe for the transposed int8 engine: tcgen05.mma kind::i8 with the A
+// operand in TMEM ("ts": lanes = M rows, 4 int8 per 32-bit column) and B in
+// shared memory (K-major, no swizzle).  Checks (1) correctness against a CPU
+// GEMM for M = 128 and N in {16, 24, 32, 48, 64} with s8/u8 B, (2) cycles per
+// MMA (1024 back-to-back MMAs, clock64) in TS mode vs SS mode.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/i8t_probe scripts/i8t_probe.cu
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e = (x);                                                               \
+        if (e != cudaSuccess) {                                                            \
+            printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+            exit(1);                                                                       \
+        }                                                                                  \
+    } while (0)
+
+__device__ __forceinline__ uint32_t saddr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+constexpr int KB = 32;  // K bytes per MMA
+
+__device__ __forceinline__ uint32_t kmajor(int row, int k, uint32_t sbo)
+{
+    return (uint32_t)(row >> 3) * sbo + (uint32_t)(k >> 4) * 128u + (uint32_t)(row & 7) * 16u + (uint32_t)(k & 15);
+}
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t a, uint32_t lbo, uint32_t sbo)
+{
+    return (uint64_t)((a & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) | (1ull << 46);
+}
+
+__device__ __forceinline__ uint32_t idesc(int m, int n, bool a_s, bool b_s)
+{
+    return (2u << 4) | ((a_s ? 1u : 0u) << 7) | ((b_s ? 1u : 0u) << 10) | ((uint32_t)(n >> 3) << 17) |
+           ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+__device__ __forceinline__ void commit(uint64_t *bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void wait_bar(uint64_t *bar, uint32_t ph)
+{
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(saddr(bar)), "r"(ph)
+            : "memory");
+}
+
+// A: [128][32] bytes (row-major m, k), B: [n][32] bytes (row n, k), D: [128][n] int32
+__global__ void probe(const int8_t *A, const int8_t *B, int n, int b_signed, int a_signed, int reps, int mode,
+                      int *D, long long *cycles)
+{
+    __shared__ __align__(1024) unsigned char sB[64 * KB];
+    __shared__ __align__(1024) unsigned char sA[128 * KB];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t sbo = (KB / 16) * 128;
+    for (int i = tid; i < n * KB; i += blockDim.x) sB[kmajor(i / KB, i % KB, sbo)] = (unsigned char)B[i];
+    for (int i = tid; i < 128 * KB; i += blockDim.x) sA[kmajor(i / KB, i % KB, sbo)] = (unsigned char)A[i];
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(saddr(&tbase)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm = tbase;
+    const uint32_t a_col = 256;  // A lives in columns [256, 264)
+    // each warp writes its lane quarter of A: row m = 32*warp + lane, 8 columns
+    if (warp < 4) {
+        const int m = 32 * warp + lane;
+        uint32_t v[8];
+        for (int j = 0; j < 8; j++) {
+            uint32_t w = 0;
+            for (int b = 0; b < 4; b++) w |= (uint32_t)(uint8_t)A[m * KB + 4 * j + b] << (8 * b);
+            v[j] = w;
+        }
+        const uint32_t ta = tm + ((uint32_t)(32 * warp) << 16) + a_col;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "r"(v[0]),
+                     "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) {
+        const uint64_t bd = sdesc(saddr(sB), 128, sbo), ad = sdesc(saddr(sA), 128, sbo);
+        const uint32_t id = idesc(128, n, a_signed, b_signed);
+        long long t0 = clock64();
+        if (lane == 0) {
+            for (int r = 0; r < reps; r++) {
+                if (mode == 0)
+                    mma_ts(tm, tm + a_col, bd, id, r > 0);
+                else
+                    mma_ss(tm, ad, bd, id, r > 0);
+            }
+            commit(&bar);
+        }
+        __syncwarp();
+        wait_bar(&bar, 0);
+        long long t1 = clock64();
+        if (lane == 0) cycles[0] = t1 - t0;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp < 4) {
+        const int m = 32 * warp + lane;
+        for (int c = 0; c < n; c += 8) {
+            uint32_t v[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                           "=r"(v[7])
+                         : "r"(tm + ((uint32_t)(32 * warp) << 16) + c));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            for (int j = 0; j < 8 && c + j < n; j++) D[m * n + c + j] = (int)v[j];
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+    }
+}
+
+int main()
+{
+    int8_t *dA, *dB;
+    int *dD;
+    long long *dc;
+    CK(cudaMalloc(&dA, 128 * KB));
+    CK(cudaMalloc(&dB, 64 * KB));
+    CK(cudaMalloc(&dD, 128 * 64 * 4));
+    CK(cudaMalloc(&dc, 8));
+    std::vector<int8_t> A(128 * KB), B(64 * KB);
+    srand(7);
+    for (auto &x : A) x = (int8_t)(rand() & 0xFF);
+    for (auto &x : B) x = (int8_t)(rand() & 0xFF);
+    CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice));
+    int ns[] = {16, 24, 32, 48, 64};
+    for (int mode = 0; mode < 2; mode++)
+        for (int n : ns)
+            for (int bs = 0; bs < 2; bs++) {
+                for (int reps : {1, 1024}) {
+                    CK(cudaMemset(dD, 0, 128 * 64 * 4));
+                    probe<<<1, 128>>>(dA, dB, n, bs, 0, reps, mode, dD, dc);
+                    cudaError_t e = cudaDeviceSynchronize();
+                    if (e != cudaSuccess) {
+                        printf("mode %s n=%d b_signed=%d: launch failed: %s\n", mode ? "ss" : "ts", n, bs,
+                               cudaGetErrorString(e));
+                        return 1;
+                    }
+                    std::vector<int> D(128 * n);
+                    long long cyc;
+                    CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+                    CK(cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost));
+                    long long bad = 0;
+                    for (int m = 0; m < 128; m++)
+                        for (int j = 0; j < n; j++) {
+                            long long s = 0;
+                            for (int k = 0; k < KB; k++) {
+                                const int a = (uint8_t)A[m * KB + k];
+                                const int b = bs ? (int)B[j * KB + k] : (int)(uint8_t)B[j * KB + k];
+                                s += (long long)a * b;
+                            }
+                            s *= reps;
+                            if ((int)s != D[m * n + j]) bad++;
+                        }
+                    printf("mode %s n=%2d b_signed=%d reps=%4d: %s (%lld bad)  cycles/mma=%.2f\n", mode ? "ss" : "ts",
+                           n, bs, reps, bad ? "WRONG" : "ok", bad, (double)cyc / reps);
+                }
+            }
+    return 0;
+}

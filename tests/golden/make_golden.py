@@ -3,7 +3,7 @@
 Run in the build container only (the reference does not exist on GPU boxes):
 
     NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
-        python tests/golden/make_golden.py [qreg]
+        python tests/golden/make_golden.py [qreg|gates]
 
 It imports ``shorsim`` from /root/reference/pkg/src (read-only; the numba cache
 is redirected to /tmp so nothing is written into the reference tree) and
@@ -269,9 +269,36 @@ def qreg_dumps():
     (OUT / "qreg_dumps.json").write_text(json.dumps(out, indent=1))
 
 
+def gates():
+    """The reference's gate primitives and gate-level QFT (qft.py:164-231) on
+    random states: outputs for a bitwise check of the device gate kernels."""
+    rng = np.random.default_rng(1434)
+    out = {}
+    q = 64
+    z = rng.standard_normal(q) + 1j * rng.standard_normal(q)
+    z[5] = complex(-0.0, -0.0)  # signed zeros through the complex products
+    z[9] = complex(0.0, -0.0)
+    out["state64"] = z
+    for b in range(6):
+        out[f"hadamard_{b}"] = qft.apply_hadamard(z, b)
+    for c, t, ang in [(0, 1, 0.7), (5, 2, -1.3), (3, 4, 2.0 * np.pi / 8), (1, 5, 1e-3)]:
+        out[f"cphase_{c}_{t}"] = qft.apply_controlled_phase(z, c, t, ang)
+    out["bitrev64"] = qft.bit_reverse_permute(z)
+    for w in (1, 4, 8, 12):
+        s = rng.standard_normal(1 << w) + 1j * rng.standard_normal(1 << w)
+        s /= np.linalg.norm(s)
+        out[f"circuit_in_{w}"] = s
+        out[f"circuit_out_{w}"] = qft.circuit_qft(s)
+    np.savez_compressed(OUT / "gates.npz", **out)
+    print("gates.npz written", flush=True)
+
+
 def main():
     if sys.argv[1:] == ["qreg"]:
         qreg_dumps()
+        return
+    if sys.argv[1:] == ["gates"]:
+        gates()
         return
     t0 = time.time()
     k = kats()
@@ -291,6 +318,7 @@ def main():
     smp = sampling()
     np.savez_compressed(OUT / "sampling.npz", state=smp["state"], draws=np.array(smp["draws"]))
     qreg_dumps()
+    gates()
     print(f"done in {time.time() - t0:.1f}s")
 
 
