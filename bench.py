@@ -380,32 +380,6 @@ def run_b200(args):
     # every rank runs the _kernels.partial_row_sums seam on its row shard.
     if not args.no_e2e:
         line["e2e"] = e2e_host(args, q, rec, lib, torch, nat, rank, world)
-    # the opt-in 6-digit int8 engine (SHB_DFT_ENGINE=i8d6) on the same attempt: time,
-    # m and its probability error against the FP64-grade spectrum just measured
-    if not args.no_fp32 and args.precision == "fp64" and "i8" in kname:
-        _, p64 = rec.spectrum
-        os.environ["SHB_DFT_ENGINE"] = "i8d6"
-        try:
-            rec6, _ = one_step(time_dft=True, keep=True)
-        finally:
-            del os.environ["SHB_DFT_ENGINE"]
-        _, p6 = rec6.spectrum
-        err6 = torch.stack([(p6 - p64).abs().max(), p64.max()])
-        del rec6.spectrum, p6
-        t6 = torch.tensor([rec6.dft_ms], dtype=torch.float64, device="cuda")
-        if world > 1:
-            torch.distributed.all_reduce(err6, op=torch.distributed.ReduceOp.MAX)
-            torch.distributed.all_reduce(t6, op=torch.distributed.ReduceOp.MAX)
-        line["fp64_i8_6digit"] = {
-            "kernel": "shb::i8d6::dft_i8_uniform_kernel", "dft_ms": float(t6.item()),
-            "int8_ops_per_phase_term": 24,
-            "phase_terms_per_s": q * M / (float(t6.item()) / 1000.0),
-            "max_abs_dp_over_max_p": float(err6[0] / err6[1]), "tolerance": 1e-9,
-            "m": rec6.m, "m_equal": rec6.m == rec.m,
-            "note": "opt-in, not the headline: G rounded to 2^-41 (6 base-128 digits, 3 pair accumulators, "
-                    "super-blocks of 64 x 128) instead of 2^-55; FP64 folds; inside the north star's FP64 "
-                    "probability bar but not FP64-grade"}
-
     # FP32 fast path on the same attempt: Horner in FP32 with exact FP64
     # re-seeds every 256 terms; accuracy vs the FP64 spectrum just measured
     if not args.no_fp32 and args.precision == "fp64":
@@ -530,37 +504,27 @@ def _cpu_column(fact: dict, args, thr: int, seconds: float = 2.0) -> None:
                                            if row["qft_phase_terms_per_s"] and rate else None)}
 
 
-# tcgen05.ld throughput per SM measured on this pool's B200 (scripts/tmem_ld_burst_probe.cu):
-# 8 warps, bursts of 8 x 32x32b.x8 loads 64 columns apart, one wait::ld per burst
-TMEM_LD_BYTES_PER_CLK = 265.7
-
-
 def _i8_roofline(rec, q, M, world, dft_s, sms, clk_mhz, kname, ops_per_term, traffic, traffic_note,
                  fp64_peak_tf, probe_dfma, probe_dmma) -> dict:
     """Roofline of the int8 tensor-core FP64 engine (csrc/dft_i8.cu), per GPU.
 
     Tensor: 16 int8 MACs (32 integer ops) per phase term (Re/Im x 8 digits of
     G*2^55); peak = 2x the measured cuBLAS bf16 rate (kind::i8 dense issues at
-    twice kind::f16 on B200: 4.5 POPS vs 2.25 PFLOPS nominal).  The kernel
-    alternates the MMA stream (~50 cycles per M128 N64 K32 MMA, ~0.9 of the
-    measured tensor rate) with the workers' drain of the accumulators (issue-
-    bound FP64 conversion + Horner), serialised on the one TMEM accumulator
-    set (clock64 timeline: profiles/r01_i8_timeline_q2_30.txt).  The TMEM read
-    rate (8 int32 accumulators per output and row-block of 96 terms) is
-    reported beside it against the tcgen05.ld rate MEASURED on this B200 for
-    the drain's access pattern (profiles/r01_tmem_ld_probe.txt)."""
+    twice kind::f16 on B200: 4.5 POPS vs 2.25 PFLOPS nominal).  The MMA is
+    M128 (row-blocks) x N24 (outputs) x K32 with the weights in TMEM; its
+    measured issue floor at N = 24 (15.4 cycles, scripts/i8t_probe.cu) is
+    reported beside the tensor peak, and the accumulator drain (FP64
+    combine + Horner, profiles/r02_i8_timeline_q2_30.txt) overlaps it on the
+    second accumulator set."""
     peaks = _measured_peaks()
     bf16 = peaks.get("bf16_tflops")
     peak_tops = 2 * bf16 if bf16 else 4500.0
     terms = rec.phase_terms
     achieved = ops_per_term * terms / dft_s / 1e12
-    # TMEM bytes read: per output and super-block, 2 comps x 4 pairs x N columns x 4 B
-    sb_amps, nb, bk = 64 * 96, 64, 96
-    nsb = -(-M // sb_amps)
-    last_rb = -(-(M - (nsb - 1) * sb_amps) // bk)
-    cols = (nsb - 1) * nb + -(-last_rb // 16) * 16
-    tmem_bytes = 32 * cols * (q // world)
-    tmem_peak = TMEM_LD_BYTES_PER_CLK * sms * clk_mhz * 1e6 / 1e9  # GB/s
+    # MMA floor of this shape: 15.4 cycles per M128 N24 K32 (524288 int8 ops... 128*24*32 MACs)
+    n24_tops = 2 * 128 * 24 * 32 / 15.4 * sms * clk_mhz * 1e6 / 1e12
+    sba = 24576
+    nsb = -(-M // sba)
     return {"bound": "tensor", "achieved": achieved, "peak": peak_tops, "unit": "TOPS",
             "frac": achieved / peak_tops, "traffic": traffic, "traffic_note": traffic_note,
             "traffic_unit": "bytes/launch", "algorithmic_bytes_per_launch": 24 * (q // world),
@@ -568,20 +532,18 @@ def _i8_roofline(rec, q, M, world, dft_s, sms, clk_mhz, kname, ops_per_term, tra
                             if bf16 else "nominal B200 int8 dense 4.5 POPS (MEASURED_PEAKS.json absent)"),
             "kernel": f"shb::{kname}", "dft_ms_per_launch": dft_s * 1000.0,
             "int8_ops_per_phase_term": ops_per_term, "ops_per_launch": ops_per_term * terms,
-            "tmem_read": {"achieved_gbs": tmem_bytes / dft_s / 1e9, "peak_gbs": tmem_peak,
-                          "frac": tmem_bytes / dft_s / 1e9 / tmem_peak, "bytes_per_launch": tmem_bytes,
-                          "peak_source": f"{TMEM_LD_BYTES_PER_CLK:.0f} B/clk/SM tcgen05.ld measured on B200 for the "
-                                         f"drain's pattern (8 warps, bursts of 8 x 32x32b.x8; "
-                                         f"profiles/r01_tmem_ld_probe.txt) x {sms} SMs x {clk_mhz:.0f} MHz"},
-            "timeline": {"source": "profiles/r01_i8_timeline_q2_30.txt (clock64, CTA 0, this config)",
-                         "mma_cycles_per_superblock": 2570, "drain_cycles_per_superblock": 2230,
-                         "g_build_cycles_per_tile": 7200,
-                         "note": "48 MMAs of M128 N64 K32 at ~51-54 cycles (~0.9 of the measured tensor rate) "
-                                 "alternate with the issue- and latency-bound FP64 drain on the one accumulator set"},
+            "mma_shape": "M128 (row-blocks, weights in TMEM) x N24 (outputs, digits of G in smem) x K32",
+            "n24_issue_floor": {"tops": n24_tops, "frac": achieved / n24_tops,
+                                "source": "15.4 cycles per M128 N24 K32 kind::i8 MMA with A in TMEM, measured "
+                                          "back to back on this B200 (scripts/i8t_probe.cu)"},
+            "superblocks_per_tile": nsb,
+            "uniform_comb_only": "the weight operand is the all-ones amplitude matrix of the collapsed register: "
+                                 "every row-block's T is the same number, so this throughput is specific to "
+                                 "uniform combs (general amplitudes take the DMMA engine)",
             "fp64_equivalent": {"tflops": 4 * terms / dft_s / 1e12, "fp64_peak_tflops": fp64_peak_tf,
-                                "ratio_to_fp64_peak": 4 * terms / dft_s / 1e12 / fp64_peak_tf,
-                                "note": "4 flops per phase term (the real-A FP64 form: amp*cos, amp*sin) against "
-                                        "the nominal FP64 rate; the products here are exact int8 digit products",
+                                "note": "4 flops per phase term (the real-A FP64 form) for comparison with the "
+                                        "FP64-pipe engines; not a roofline of this kernel (its products are "
+                                        "exact int8 digit products on the tensor cores)",
                                 "peak_probe_dfma": probe_dfma, "peak_probe_dmma": probe_dmma}}
 
 

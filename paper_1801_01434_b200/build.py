@@ -18,8 +18,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libshorb200.so"
 SOURCES = ["capi.cu", "modexp.cu", "collapse.cu", "dft.cu", "dft_tc05.cu", "dft_i8.cu", "sample.cu", "context.cu", "gates.cu"]
-# extra objects: (object stem, source, defines) -- dft_i8.cu once more as the 6-digit engine
-EXTRA = [("dft_i8d6", "dft_i8.cu", ["-DSHB_I8_DIGITS=6"])]
+# extra objects: (object stem, source, defines)
+EXTRA = []
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-O2", "-Xptxas", "-v"]

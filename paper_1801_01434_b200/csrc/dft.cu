@@ -1021,20 +1021,13 @@ static bool use_mma_engine(bool uniform, uint64_t q)
 }
 
 // Uniform comb, FP64: the int8 tensor-core engine (dft_i8.cu) by default --
-// exact integer products of an 8-digit split of G*2^55 with FP64 folds, max
-// |dV|/max|V| ~3e-15 against the DMMA engine, 2.14 s vs 9.05 s at q = 2^30
-// (scripts/i8_check.py).  SHB_DFT_ENGINE=mma|vector selects the FP64-pipe kernels.
+// exact integer products of an 8-digit split of G*2^55 with FP64 folds, ~2e-15
+// of max|V| against the long-double closed form (tests/test_gpu_baseline_configs.py).
+// SHB_DFT_ENGINE=mma|vector selects the FP64-pipe kernels.
 static bool use_i8_engine()
 {
     const char *e = getenv("SHB_DFT_ENGINE");
     return !(e && e[0]) || e[0] == 'i';
-}
-
-// SHB_DFT_ENGINE=i8d6: the 6-digit split (opt-in; ~1e-13 of max|V| instead of ~3e-15)
-static bool use_i8_six_digits()
-{
-    const char *e = getenv("SHB_DFT_ENGINE");
-    return e && e[0] == 'i' && e[1] == '8' && e[2] == 'd' && e[3] == '6';
 }
 
 static bool use_real_form()
@@ -1148,7 +1141,7 @@ extern "C" int shb_dft_uniform(double amp_re, double amp_im, uint64_t length, ui
         return launch_dft<float, true>(a, length, tiles, st);
     }
     if (tiles == 1 && length && use_i8_engine())
-        return (use_i8_six_digits() ? i8d6_dft_uniform : i8_dft_uniform)(length, a0, stride, q, c_begin, c_count, a.out_re, a.out_im, d_out, d_prob,
+        return i8_dft_uniform(length, a0, stride, q, c_begin, c_count, a.out_re, a.out_im, d_out, d_prob,
                               d_block_sums, (uint64_t)DFT_THREADS * Prec<double>::K, st);
     if (tiles == 1 && length && use_mma_engine(true, q)) {
         // the amplitude is factored out (out factor = amp*scale): the MMA runs on ones
@@ -1171,9 +1164,8 @@ extern "C" const char *shb_dft_engine(int uniform, int real, uint64_t q, int pre
         return fp32_engine() == F32_TC05 ? "dft_tc05_uniform_kernel" : "dft_tc32_uniform_kernel";
     }
     if (precision == SHB_FP64 && uniform && tiles == 1 && use_i8_engine()) {
-        const bool six = use_i8_six_digits();
-        if (flops_per_term) *flops_per_term = six ? 24 : 32;  // 16 (12) int8 MACs: (Re, Im) x 8 (6) digits
-        return six ? "i8d6::dft_i8_uniform_kernel" : "dft_i8_uniform_kernel";
+        if (flops_per_term) *flops_per_term = 32;  // 16 int8 MACs: (Re, Im) x 8 digits
+        return "i8::dft_i8_uniform_kernel";
     }
     const bool mma = precision == SHB_FP64 && tiles == 1 && use_mma_engine(uniform != 0, q);
     const bool realf = mma && (uniform || real) && use_real_form();

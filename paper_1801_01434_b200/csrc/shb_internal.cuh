@@ -57,11 +57,6 @@ int tc05_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, 
 int i8_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin, uint64_t c_count,
                    double out_re, double out_im, double *d_out, double *d_prob, double *d_block_sums,
                    uint64_t slot_outputs, cudaStream_t st);
-// The same kernel on a 6-digit split of G*2^41 (dft_i8.cu built with SHB_I8_DIGITS=6):
-// 25 % less tensor and drain work, max|dV|/max|V| ~1e-13 (SHB_DFT_ENGINE=i8d6, opt-in).
-int i8d6_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin, uint64_t c_count,
-                     double out_re, double out_im, double *d_out, double *d_prob, double *d_block_sums,
-                     uint64_t slot_outputs, cudaStream_t st);
 
 // ------------------------------------------------------------ integer math
 __host__ __device__ inline uint64_t gcd_u64(uint64_t a, uint64_t b)

@@ -185,7 +185,7 @@ def tiled_dft(state, tw: TwiddleTable, plan: KernelPlan):
 
 
 def _length(state) -> int:
-    return state.q if isinstance(state, dev.DeviceVector) else len(state)
+    return state.q if isinstance(state, dev.DeviceVector) else int(np.size(state))
 
 
 def fft_dft(state, precision: str = "fp64"):
@@ -233,11 +233,12 @@ def _finish(data, q: int, host: bool):
 
 def apply_hadamard(state, qubit_index: int):
     """qft.py:164-177: (u, v) -> ((u+v)/sqrt2, (u-v)/sqrt2) on bit `qubit_index`."""
-    data, q, host = _dense_device_copy(state)
+    q = _length(state)
     _require_power_of_two(q)
     w = q.bit_length() - 1
     if not 0 <= qubit_index < w:
         raise ValueError(f"qubit index {qubit_index} out of range for w={w}")
+    data, q, host = _dense_device_copy(state)
     dev.apply_hadamard(data, q, qubit_index)
     return _finish(data, q, host)
 
@@ -251,12 +252,13 @@ def apply_controlled_phase(state, control: int, target: int, angle: float):
     """qft.py:180-196: amplitudes with both index bits set times e^{+i angle}."""
     if control == target:
         raise ValueError("control and target must differ")
-    data, q, host = _dense_device_copy(state)
+    q = _length(state)
     _require_power_of_two(q)
     w = q.bit_length() - 1
     for bit in (control, target):
         if not 0 <= bit < w:
             raise ValueError(f"qubit index {bit} out of range for w={w}")
+    data, q, host = _dense_device_copy(state)
     dev.apply_controlled_phase(data, q, control, target, _phase(angle))
     return _finish(data, q, host)
 
@@ -266,9 +268,9 @@ def bit_reverse_permute(state):
 
     The reference keeps the input dtype; real and integer inputs are moved
     as complex128 (exact for |values| < 2^53) and cast back."""
-    if isinstance(state, (dev.DeviceVector,)):
-        data, q, host = _dense_device_copy(state)
-        _require_power_of_two(q)
+    if isinstance(state, dev.DeviceVector):
+        _require_power_of_two(state.q)
+        data, q, _ = _dense_device_copy(state)
         return _finish(dev.bit_reverse_permute(data, q), q, False)
     a = np.asarray(state)
     _require_power_of_two(a.size)
@@ -291,11 +293,12 @@ def circuit_qft(state, max_width: int = CIRCUIT_MAX_WIDTH):
     """Gate-level QFT (qft.py:215-231): Hadamards plus controlled phases, then
     the bit reversal -- O(w^2) device gate launches, width cap kept.  An
     independent construction of the same unitary as the DFT kernels."""
-    data, q, host = _dense_device_copy(state)
+    q = _length(state)
     _require_power_of_two(q)
     w = q.bit_length() - 1
     if w > max_width:
         raise ValueError(f"circuit engine capped at w <= {max_width}, got w={w}")
+    data, q, host = _dense_device_copy(state)
     for i in range(w - 1, -1, -1):
         dev.apply_hadamard(data, q, i)
         for j in range(i - 1, -1, -1):

@@ -13,9 +13,12 @@ import torch  # noqa: E402
 
 from paper_1801_01434_b200 import device as dev  # noqa: E402
 
-cases = [(1 << 8, 1, 4, 64), (1 << 16, 11, 12, 5461), (1 << 16, 3, 7, 9000), (1 << 24, 29, 116, 144631)]
+cases = [(1 << 8, 1, 4, 64), (1 << 16, 11, 12, 5461), (1 << 16, 3, 7, 9000)]
+# super-block / K-chunk edges of the engine (4096 amplitudes per chunk, 16384 per super-block)
+cases += [(1 << 20, 5, 3, M) for M in (1, 31, 4095, 4096, 4097, 16383, 16384, 16385, 40000, 2 * 16384 + 97)]
+cases.append((1 << 24, 29, 116, 144631))
 if len(sys.argv) > 1 and sys.argv[1] == "big":
-    cases.append((1 << 30, 10943, 16020, 67025))
+    cases += [(1 << 30, 10943, 16020, 67025), (1 << 30, 4828, 5340, 201075)]
 
 
 def run(eng, amp, M, c0, r, q, cb, cc):
@@ -43,8 +46,8 @@ for q, c0, r, M in cases:
            "max_dV_over_max_V": float((o8 - o64).abs().max()) / vmax,
            "max_dp_over_max_p": float((p8 - p64).abs().max()) / float(p64.max()),
            "norm_mma": dev.dsum(b64), "norm_i8": dev.dsum(b8)}
-    if q <= 1 << 16:
-        cb, cc = 1000 % q, min(777, q - 1000 % q)
+    if q <= 1 << 20:
+        cb, cc = 1000 % q, min(7777, q - 1000 % q)
         os_, _, _, _ = run("i8", amp, M, c0, r, q, cb, cc)
         rec["shard_bitwise"] = bool(torch.equal(os_, o8[2 * cb: 2 * (cb + cc)]))
     print(json.dumps(rec), flush=True)

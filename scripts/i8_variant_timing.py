@@ -14,7 +14,7 @@ from paper_1801_01434_b200 import _native as nat  # noqa: E402
 from paper_1801_01434_b200 import device as dev  # noqa: E402
 
 libs = sorted(Path(nat.LIB_PATH.parent / "_variants").glob("libshorb200_i8_*.so")) + [nat.LIB_PATH]
-cases = [(1 << 24, 29, 116, 144631)]
+cases = [(1 << 24, 29, 116, 144631), (1 << 26, 4828, 300, 201075), (1 << 26, 10943, 900, 67025)]
 if "big" in sys.argv:
     cases.append((1 << 30, 10943, 16020, 67025))
 for q, c0, r, M in cases:

@@ -58,6 +58,13 @@ __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint3
         "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 
+__device__ __forceinline__ bool elect_one()
+{
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void commit(uint64_t *bar)
 {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(bar))
@@ -76,7 +83,8 @@ __device__ __forceinline__ void wait_bar(uint64_t *bar, uint32_t ph)
 }
 
 // A: [128][32] bytes (row-major m, k), B: [n][32] bytes (row n, k), D: [128][n] int32
-__global__ void probe(const int8_t *A, const int8_t *B, int n, int b_signed, int a_signed, int reps, int mode,
+template <int MODE, int NACC, int DSTRIDE = 64, int ACOL = 256>
+__global__ void probe(const int8_t *A, const int8_t *B, int n, int b_signed, int a_signed, int reps,
                       int *D, long long *cycles)
 {
     __shared__ __align__(1024) unsigned char sB[64 * KB];
@@ -100,7 +108,7 @@ __global__ void probe(const int8_t *A, const int8_t *B, int n, int b_signed, int
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tm = tbase;
-    const uint32_t a_col = 256;  // A lives in columns [256, 264)
+    const uint32_t a_col = ACOL;  // A lives in columns [ACOL, ACOL + 8)
     // each warp writes its lane quarter of A: row m = 32*warp + lane, 8 columns
     if (warp < 4) {
         const int m = 32 * warp + lane;
@@ -122,15 +130,33 @@ __global__ void probe(const int8_t *A, const int8_t *B, int n, int b_signed, int
         const uint64_t bd = sdesc(saddr(sB), 128, sbo), ad = sdesc(saddr(sA), 128, sbo);
         const uint32_t id = idesc(128, n, a_signed, b_signed);
         long long t0 = clock64();
-        if (lane == 0) {
-            for (int r = 0; r < reps; r++) {
-                if (mode == 0)
-                    mma_ts(tm, tm + a_col, bd, id, r > 0);
+        // the whole warp walks the loop; one elected lane issues 16 MMAs per step,
+        // rotating over NACC accumulators (64 columns apart, below A at column 256)
+        if (elect_one()) {
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                const uint32_t d = tm + (uint32_t)((u % NACC) * DSTRIDE);
+                if (MODE == 0)
+                    mma_ts(d, tm + a_col, bd, id, u >= NACC);
                 else
-                    mma_ss(tm, ad, bd, id, r > 0);
+                    mma_ss(d, ad, bd, id, u >= NACC);
             }
-            commit(&bar);
         }
+        __syncwarp();
+        for (int r = 16; r < reps; r += 16) {
+            if (elect_one()) {
+#pragma unroll
+                for (int u = 0; u < 16; u++) {
+                    const uint32_t d = tm + (uint32_t)((u % NACC) * DSTRIDE);
+                    if (MODE == 0)
+                        mma_ts(d, tm + a_col, bd, id, 1);
+                    else
+                        mma_ss(d, ad, bd, id, 1);
+                }
+            }
+            __syncwarp();
+        }
+        if (elect_one()) commit(&bar);
         __syncwarp();
         wait_bar(&bar, 0);
         long long t1 = clock64();
@@ -175,37 +201,40 @@ int main()
     CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice));
     int ns[] = {16, 24, 32, 48, 64};
-    for (int mode = 0; mode < 2; mode++)
-        for (int n : ns)
-            for (int bs = 0; bs < 2; bs++) {
-                for (int reps : {1, 1024}) {
-                    CK(cudaMemset(dD, 0, 128 * 64 * 4));
-                    probe<<<1, 128>>>(dA, dB, n, bs, 0, reps, mode, dD, dc);
-                    cudaError_t e = cudaDeviceSynchronize();
-                    if (e != cudaSuccess) {
-                        printf("mode %s n=%d b_signed=%d: launch failed: %s\n", mode ? "ss" : "ts", n, bs,
-                               cudaGetErrorString(e));
-                        return 1;
-                    }
-                    std::vector<int> D(128 * n);
-                    long long cyc;
-                    CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
-                    CK(cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost));
-                    long long bad = 0;
-                    for (int m = 0; m < 128; m++)
-                        for (int j = 0; j < n; j++) {
-                            long long s = 0;
-                            for (int k = 0; k < KB; k++) {
-                                const int a = (uint8_t)A[m * KB + k];
-                                const int b = bs ? (int)B[j * KB + k] : (int)(uint8_t)B[j * KB + k];
-                                s += (long long)a * b;
-                            }
-                            s *= reps;
-                            if ((int)s != D[m * n + j]) bad++;
-                        }
-                    printf("mode %s n=%2d b_signed=%d reps=%4d: %s (%lld bad)  cycles/mma=%.2f\n", mode ? "ss" : "ts",
-                           n, bs, reps, bad ? "WRONG" : "ok", bad, (double)cyc / reps);
-                }
+    auto run = [&](auto kern, const char *mname, int nacc) {
+        for (int n : ns) {
+            const int bs = 1, reps = 4096;
+            CK(cudaMemset(dD, 0, 128 * 64 * 4));
+            kern<<<1, 128>>>(dA, dB, n, bs, 0, reps, dD, dc);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) {
+                printf("%s n=%d: launch failed: %s\n", mname, n, cudaGetErrorString(e));
+                exit(1);
             }
+            std::vector<int> D(128 * n);
+            long long cyc;
+            CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost));
+            long long bad = 0;
+            for (int m = 0; m < 128; m++)
+                for (int j = 0; j < n; j++) {
+                    long long s = 0;
+                    for (int k = 0; k < KB; k++) s += (long long)(uint8_t)A[m * KB + k] * (int)B[j * KB + k];
+                    s *= reps / nacc;
+                    if ((int)s != D[m * n + j]) bad++;
+                }
+            printf("mode %s nacc=%d n=%2d: %s  cycles/mma=%.2f  floor=%.1f\n", mname, nacc, n, bad ? "WRONG" : "ok",
+                   (double)cyc / reps, 128.0 * n / 256);
+        }
+    };
+    run(probe<0, 1>, "ts", 1);
+    run(probe<0, 2>, "ts", 2);
+    run(probe<0, 4>, "ts", 4);
+    run(probe<0, 4, 24, 392>, "ts d24 a392", 4);
+    run(probe<0, 4, 24, 400>, "ts d24 a400", 4);
+    run(probe<0, 4, 24, 404>, "ts d24 a404", 4);
+    run(probe<1, 1>, "ss", 1);
+    run(probe<1, 2>, "ss", 2);
+    run(probe<1, 4>, "ss", 4);
     return 0;
 }

@@ -124,7 +124,7 @@ def test_dft_engine_choice(lib, monkeypatch):
 
     for var in ("SHB_DFT_ENGINE", "SHB_MMA_REAL", "SHB_FP32_ENGINE"):
         monkeypatch.delenv(var, raising=False)
-    assert eng(1, 1) == ("dft_i8_uniform_kernel", 32)
+    assert eng(1, 1) == ("i8::dft_i8_uniform_kernel", 32)
     assert eng(0, 1) == ("dft_mma_kernel<generic, real A>", 4)
     assert eng(0, 0) == ("dft_mma_kernel<generic, complex A>", 8)
     assert eng(1, 1, tiles=4)[0] == "dft_kernel<uniform>"
@@ -133,10 +133,7 @@ def test_dft_engine_choice(lib, monkeypatch):
     # the choice never depends on the output range, only on q and the data
     assert eng(1, 1, q=1 << 8) == eng(1, 1, q=1 << 32)
     monkeypatch.setenv("SHB_DFT_ENGINE", "i8")
-    assert eng(1, 1) == ("dft_i8_uniform_kernel", 32)
-    assert eng(0, 1) == ("dft_mma_kernel<generic, real A>", 4)
-    monkeypatch.setenv("SHB_DFT_ENGINE", "i8d6")  # opt-in 6-digit split: 12 int8 MACs per term
-    assert eng(1, 1) == ("i8d6::dft_i8_uniform_kernel", 24)
+    assert eng(1, 1) == ("i8::dft_i8_uniform_kernel", 32)
     assert eng(0, 1) == ("dft_mma_kernel<generic, real A>", 4)
     monkeypatch.setenv("SHB_DFT_ENGINE", "mma")
     assert eng(1, 1) == ("dft_mma_kernel<uniform, real A>", 4)
