@@ -91,7 +91,12 @@ constexpr int FOLD_STRIDE = NO + 1;       // complex per row-block row of the fo
 constexpr int FOLD_BYTES = LANES * FOLD_STRIDE * 16;
 constexpr int SMEM_BYTES = 2 * G_BYTES + FOLD_BYTES;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
-constexpr int G_ITEMS = NO * KCH;          // (output, K-chunk) items of a tile's G: 32 k each
+#ifndef SHB_I8_GSPAN
+#define SHB_I8_GSPAN 32
+#endif
+constexpr int GSPAN = SHB_I8_GSPAN;        // k per G item (16 or 32)
+static_assert(GSPAN == 16 || GSPAN == 32, "G item span");
+constexpr int G_ITEMS = NO * BK / GSPAN;   // (output, k-span) items of a tile's G
 constexpr int DRAIN_WARPS = 12, G_WARPS = (G_ITEMS + 31) / 32;
 constexpr int DRAIN_THREADS = DRAIN_WARPS * 32, G_THREADS = G_WARPS * 32;
 constexpr int MMA_WARP = DRAIN_WARPS + G_WARPS;
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
         }
     } else if (warp >= DRAIN_WARPS) {
         // ------------------------------------------------------------ G builders
-        // thread -> items (output n, 16-k group kg); k = kg*16 + e, K-chunk kc = k / 32
+        // thread -> item (output n, k-span ks of GSPAN k inside one K-chunk kc = ks*GSPAN / 32)
         const int gt = tid - DRAIN_THREADS;
         uint32_t it = 0;
         for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, it++) {
@@ -372,15 +377,17 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 tconst[gb][kind][nn] = v;
             }
             if (gt < G_ITEMS) {
-                const int n = gt % NO, kc = gt / NO;
+                const int n = gt % NO, ks = gt / NO;  // k-span ks covers k = ks*GSPAN ... + GSPAN - 1
+                const int kc = ks * GSPAN / KC;
                 const uint64_t c = p.c_begin + t * NO + n;
                 // G[k, c] = e^{+2 pi i (kc*4096 + kk) stride c / q}, kk < 32: exact sincospi at
                 // kk = 0 and kk = 16, FP64 rotation by e^{+2 pi i stride c / q} in between
                 const double2 w = phase((p.stride * c) & qmask, q, p.two_over_q);
-                unsigned char *buf = sG + gb * G_BYTES + kmajor(n, kc * KC);
+                unsigned char *buf = sG + gb * G_BYTES + kmajor(n, ks * GSPAN);
 #pragma unroll 1
-                for (int k16 = 0; k16 < 2; k16++) {
-                    double2 g = phase(((uint64_t)(kc * CHUNK_AMPS + 16 * k16) * p.stride * c) & qmask, q,
+                for (int k16 = 0; k16 < GSPAN / 16; k16++) {
+                    const int kk0 = (ks * GSPAN) % KC + 16 * k16;
+                    double2 g = phase(((uint64_t)(kc * CHUNK_AMPS + kk0) * p.stride * c) & qmask, q,
                                       p.two_over_q);
 #pragma unroll
                     for (int half = 0; half < 2; half++) {
@@ -390,7 +397,11 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                         for (int e = 0; e < 8; e++) {
 #pragma unroll
                             for (int comp = 0; comp < 2; comp++) {
-                                const long long X = __double2ll_rn((comp ? g.y : g.x) * 0x1p55);
+                                // X = rint(G 2^55): the power-of-two scale as an exponent add on the
+                                // bit pattern (INT pipe; exact for every normal G, and 0 maps to a
+                                // tiny normal that rounds to 0) instead of a DMUL on the busy FP64 pipe
+                                const long long X = __double2ll_rn(__longlong_as_double(
+                                    __double_as_longlong(comp ? g.y : g.x) + (55LL << 52)));
                                 const int d0 = (int)(X >> 49);
                                 const unsigned long long R = (unsigned long long)(X - ((long long)d0 << 49));
                                 const uint32_t hi28 = (uint32_t)(R >> 21), lo21 = (uint32_t)R & 0x1FFFFFu;
