@@ -213,6 +213,27 @@ int shb_cumsum_search_from(const double *d_prob, uint64_t count, double s_in,
 int shb_sample_index(const double *d_prob, uint64_t count, double u,
                      uint64_t *index, double *total, void *stream);
 
+/* Split form of the sequential cumsum, for a vector sharded over ranks or
+ * devices (the sharded Born-rule read, distributed.py / shb_sample):
+ *   shb_cumsum_records  -- per-tile binade records from a HINT of the running
+ *                          value entering this shard (parallel on every shard;
+ *                          the result stays exact whatever the hint);
+ *   shb_cumsum_walk     -- the exact walk from the exact s_in: *s_out, and the
+ *                          exact running value at every tile start in d_tile_S;
+ *                          this is the only step that chains shard to shard;
+ *   shb_cumsum_find     -- searchsorted(cumsum, target, "right") in the shard
+ *                          from d_tile_S and the shard's total (*index = count
+ *                          when no running value exceeds target).
+ * Buffers: d_recs holds shb_cumsum_tiles(count) * shb_cumsum_record_bytes()
+ * bytes, d_tile_S shb_cumsum_tiles(count) doubles. */
+uint64_t shb_cumsum_tiles(uint64_t count);
+uint64_t shb_cumsum_record_bytes(void);
+int shb_cumsum_records(const double *d_prob, uint64_t count, double s_hint, void *d_recs, void *stream);
+int shb_cumsum_walk(const double *d_prob, uint64_t count, const void *d_recs, double s_in,
+                    double *d_tile_S, double *s_out, void *stream);
+int shb_cumsum_find(const double *d_prob, uint64_t count, const double *d_tile_S, double total,
+                    double target, uint64_t *index, void *stream);
+
 /* ------------------------------------------------- host-buffer drop-ins
  * These own their device memory (current device) and take HOST buffers:
  * the C-level equivalents of the reference calls, for FFI users.
@@ -238,8 +259,9 @@ int shb_partial_row_sums_host(double *out, const double *state,
  * pointers.  The register is sharded over the handle's
  * devices: part 2 (residues) by index a, the spectrum by output c.  One host
  * thread drives every shard; the only cross-shard exchanges are the class
- * counts (host sum), the support geometry (host gcd) and, for sampling, a
- * peer copy of the probabilities to the first shard's device.
+ * counts (host sum), the support geometry (host gcd) and, for sampling, the
+ * exact running value of the sequential CDF carried shard to shard (the
+ * split cumsum above: records on every shard at once, then the walk).
  *
  * Stage order (each call checks it, SHB_EINVAL otherwise):
  *   shb_init -> shb_ctx_modexp          init_uniform + entangle_modexp (qstate.py:56-83)

@@ -57,6 +57,11 @@ SIGNATURES = {
     "shb_cumsum_total_from": ([_vp, _u64, _f64, _PF64, _vp], _i32),
     "shb_cumsum_search_from": ([_vp, _u64, _f64, _f64, _P64, _vp], _i32),
     "shb_sample_index": ([_vp, _u64, _f64, _P64, _PF64, _vp], _i32),
+    "shb_cumsum_tiles": ([_u64], _u64),
+    "shb_cumsum_record_bytes": ([], _u64),
+    "shb_cumsum_records": ([_vp, _u64, _f64, _vp, _vp], _i32),
+    "shb_cumsum_walk": ([_vp, _u64, _vp, _f64, _vp, _PF64, _vp], _i32),
+    "shb_cumsum_find": ([_vp, _u64, _vp, _f64, _f64, _P64, _vp], _i32),
     "shb_dense_dft_host": ([_vp, _u64, _u32, _i32, _vp], _i32),
     "shb_partial_row_sums_host": ([_vp, _vp, _vp, _u64, _u64, _u64, _u64, _u64], _i32),
     "shb_init": ([_i32, ctypes.POINTER(_vp)], _i32),

@@ -35,6 +35,8 @@ struct Shard {
     uint64_t m = 0;
     double *spec = nullptr, *prob = nullptr, *bsums = nullptr;
     uint64_t nb = 0;
+    void *recs = nullptr;      // split-cumsum records of this shard's probabilities
+    double *tile_S = nullptr;  // exact running value at each of its tile starts
 };
 
 struct DeviceGuard {
@@ -88,7 +90,6 @@ struct shb_ctx {
     uint64_t M = 0, a0 = 0, stride = 1, len = 0;
     double amp = 0.0;
     int precision = SHB_FP64;
-    double *gather = nullptr;  // float64[q] on shard 0's device (multi-shard sampling)
 
     void release_from(int stage_keep)
     {
@@ -98,6 +99,8 @@ struct shb_ctx {
                 dev_free(s.dev, s.spec);
                 dev_free(s.dev, s.prob);
                 dev_free(s.dev, s.bsums);
+                dev_free(s.dev, s.recs);
+                dev_free(s.dev, s.tile_S);
                 s.nb = 0;
             }
             if (stage_keep < 2) {
@@ -109,7 +112,6 @@ struct shb_ctx {
                 s.counts.clear();
             }
         }
-        if (stage_keep < 3 && !sh.empty()) dev_free(sh[0].dev, gather);
         if (stage_keep < 1) {
             counted = false;
             counts.clear();
@@ -432,21 +434,54 @@ int shb_sample(shb_ctx *c, double u, uint64_t *m_out)
     SHB_TRY(shb_norm(c, &norm));
     const double tol = c->precision == SHB_FP64 ? 1e-9 : 1e-4;  // _NORM_TOL (qstate.py:17) / FP32 accuracy
     if (!(fabs(norm - 1.0) <= tol)) return set_error(SHB_EINVAL, "register is not normalized (|amp| = %.17g)", norm);
+    // The exact sequential CDF over the c-shards without moving the
+    // probabilities: every shard builds its binade records at once (from a hint
+    // of the value entering it: the approximate sums of the shards before it),
+    // then the exact running value is carried shard to shard through the
+    // records-driven walk, and the shard that first passes u * total is
+    // searched (the same split as distributed._sharded_sample).
     DeviceGuard g;
-    Shard &s0 = c->sh[0];
-    const double *prob = s0.prob;
-    if (c->sh.size() > 1) {
-        SHB_TRY_CUDA(cudaSetDevice(s0.dev));
-        if (!c->gather) SHB_TRY(dev_alloc((void **)&c->gather, c->q * 8));
-        for (auto &s : c->sh) {
-            if (!s.c_count) continue;
-            SHB_TRY_CUDA(cudaMemcpyPeerAsync(c->gather + s.c_begin, s0.dev, s.prob, s.dev, s.c_count * 8, s0.st));
-        }
-        prob = c->gather;
+    std::vector<double> approx(c->sh.size(), 0.0);
+    for (size_t i = 0; i < c->sh.size(); i++) {
+        Shard &s = c->sh[i];
+        if (!s.c_count) continue;
+        SHB_TRY_CUDA(cudaSetDevice(s.dev));
+        SHB_TRY(shb_sum(s.prob, s.c_count, &approx[i], s.st));
     }
-    SHB_TRY_CUDA(cudaSetDevice(s0.dev));
-    uint64_t idx = 0;
-    SHB_TRY(shb_sample_index(prob, c->q, u, &idx, nullptr, s0.st));
+    double hint = 0.0;
+    for (size_t i = 0; i < c->sh.size(); i++) {
+        Shard &s = c->sh[i];
+        if (s.c_count) {
+            SHB_TRY_CUDA(cudaSetDevice(s.dev));
+            const uint64_t nt = shb_cumsum_tiles(s.c_count);
+            if (!s.recs) SHB_TRY(dev_alloc(&s.recs, nt * shb_cumsum_record_bytes()));
+            if (!s.tile_S) SHB_TRY(dev_alloc((void **)&s.tile_S, nt * sizeof(double)));
+            SHB_TRY(shb_cumsum_records(s.prob, s.c_count, hint, s.recs, s.st));  // async on every device
+        }
+        hint += approx[i];
+    }
+    std::vector<double> enter(c->sh.size(), 0.0), leave(c->sh.size(), 0.0);
+    double run = 0.0;
+    for (size_t i = 0; i < c->sh.size(); i++) {
+        Shard &s = c->sh[i];
+        enter[i] = run;
+        if (s.c_count) {
+            SHB_TRY_CUDA(cudaSetDevice(s.dev));
+            SHB_TRY(shb_cumsum_walk(s.prob, s.c_count, s.recs, run, s.tile_S, &run, s.st));
+        }
+        leave[i] = run;
+    }
+    const double target = u * run;  // s.uniform() * cum[-1] (qstate.py:113)
+    uint64_t idx = c->q;
+    for (size_t i = 0; i < c->sh.size(); i++) {
+        Shard &s = c->sh[i];
+        if (!s.c_count || !(leave[i] > target)) continue;
+        SHB_TRY_CUDA(cudaSetDevice(s.dev));
+        uint64_t local = 0;
+        SHB_TRY(shb_cumsum_find(s.prob, s.c_count, s.tile_S, leave[i], target, &local, s.st));
+        idx = s.c_begin + local;
+        break;
+    }
     *m_out = idx < c->q - 1 ? idx : c->q - 1;
     return SHB_OK;
 }

@@ -541,31 +541,55 @@ extern "C" int shb_sum(const double *d_x, uint64_t count, double *out, void *str
     return SHB_OK;
 }
 
-// exact walk over all tiles -> (total, exact running sum at every tile start)
-static int seq_total(const double *d_prob, uint64_t count, double s_in, double *tile_S, double *total_host,
-                     cudaStream_t st)
+// The sequential cumsum in two parts.  (1) Records: approximate tile sums,
+// their prefix from a hint of the running value entering the vector, and per
+// tile the integer increment in the binade that prefix predicts -- all
+// parallel, and exactness does not depend on the hint (a mispredicted tile
+// is simply walked element by element).  (2) The walk: one CTA advances the
+// EXACT running sum from s_in over the records (32 tiles per warp step) and
+// writes the exact running value at every tile start.  A sharded read
+// computes (1) on every shard at once and chains only (2) from shard to shard.
+static int seq_records(const double *d_prob, uint64_t count, double s_hint, TileRec *recs, cudaStream_t st)
+{
+    const uint64_t nt = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    Scratch tsum, tstart;
+    SHB_TRY(scratch_alloc(tsum, sizeof(double) * nt, st));
+    SHB_TRY(scratch_alloc(tstart, sizeof(double) * nt, st));
+    tile_sum_kernel<<<(unsigned)nt, 256, 0, st>>>(d_prob, count, (double *)tsum.ptr);
+    SHB_LAUNCHED();
+    tile_prefix_kernel<<<1, SUM_THREADS, 0, st>>>((const double *)tsum.ptr, nt, s_hint, (double *)tstart.ptr);
+    SHB_LAUNCHED();
+    tile_rec_kernel<<<(unsigned)nt, 256, 0, st>>>(d_prob, count, (const double *)tstart.ptr, recs);
+    SHB_LAUNCHED();
+    SHB_TRY_CUDA(cudaGetLastError());
+    return SHB_OK;
+}
+
+static int seq_walk(const double *d_prob, uint64_t count, const TileRec *recs, double s_in, double *tile_S,
+                    double *total_host, cudaStream_t st)
 {
     SHB_TRY(seq_prepare());
     const uint64_t nt = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
-    Scratch tot, tsum, tstart, recs;
+    Scratch tot;
     SHB_TRY(scratch_alloc(tot, sizeof(double), st));
-    SHB_TRY(scratch_alloc(tsum, sizeof(double) * nt, st));
-    SHB_TRY(scratch_alloc(tstart, sizeof(double) * nt, st));
-    SHB_TRY(scratch_alloc(recs, sizeof(TileRec) * nt, st));
-    tile_sum_kernel<<<(unsigned)nt, 256, 0, st>>>(d_prob, count, (double *)tsum.ptr);
-    SHB_LAUNCHED();
-    tile_prefix_kernel<<<1, SUM_THREADS, 0, st>>>((const double *)tsum.ptr, nt, s_in, (double *)tstart.ptr);
-    SHB_LAUNCHED();
-    tile_rec_kernel<<<(unsigned)nt, 256, 0, st>>>(d_prob, count, (const double *)tstart.ptr, (TileRec *)recs.ptr);
-    SHB_LAUNCHED();
-    seqscan_kernel<<<1, SEQ_THREADS, seq_smem(), st>>>(d_prob, count, 0, nt, s_in, 0, 0.0,
-                                                         (const TileRec *)recs.ptr, tile_S, (double *)tot.ptr,
-                                                         nullptr);
+    seqscan_kernel<<<1, SEQ_THREADS, seq_smem(), st>>>(d_prob, count, 0, nt, s_in, 0, 0.0, recs, tile_S,
+                                                         (double *)tot.ptr, nullptr);
     SHB_LAUNCHED();
     SHB_TRY_CUDA(cudaGetLastError());
     SHB_TRY_CUDA(cudaMemcpyAsync(total_host, tot.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
     SHB_TRY_CUDA(cudaStreamSynchronize(st));
     return SHB_OK;
+}
+
+// exact walk over all tiles -> (total, exact running sum at every tile start)
+static int seq_total(const double *d_prob, uint64_t count, double s_in, double *tile_S, double *total_host,
+                     cudaStream_t st)
+{
+    const uint64_t nt = (count + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    Scratch recs;
+    SHB_TRY(scratch_alloc(recs, sizeof(TileRec) * nt, st));
+    SHB_TRY(seq_records(d_prob, count, s_in, (TileRec *)recs.ptr, st));
+    return seq_walk(d_prob, count, (const TileRec *)recs.ptr, s_in, tile_S, total_host, st);
 }
 
 extern "C" int shb_cumsum_total(const double *d_prob, uint64_t count, double *total, void *stream)
@@ -669,4 +693,36 @@ extern "C" int shb_sample_index(const double *d_prob, uint64_t count, double u, 
     if (total) *total = tot;
     const double target = u * tot;  // s.uniform() * cum[-1] (qstate.py:113)
     return search_from_tiles(d_prob, count, (const double *)cs.ptr, tot, target, index, st);
+}
+
+// ------------------------------------------------ split scan (sharded reads)
+extern "C" uint64_t shb_cumsum_tiles(uint64_t count) { return (count + SEQ_CHUNK - 1) / SEQ_CHUNK; }
+
+extern "C" uint64_t shb_cumsum_record_bytes(void) { return sizeof(TileRec); }
+
+extern "C" int shb_cumsum_records(const double *d_prob, uint64_t count, double s_hint, void *d_recs, void *stream)
+{
+    if (count == 0) return SHB_OK;
+    if (!d_prob || !d_recs) return set_error(SHB_EINVAL, "null buffer");
+    return seq_records(d_prob, count, s_hint, (TileRec *)d_recs, as_stream(stream));
+}
+
+extern "C" int shb_cumsum_walk(const double *d_prob, uint64_t count, const void *d_recs, double s_in,
+                               double *d_tile_S, double *s_out, void *stream)
+{
+    if (!s_out) return set_error(SHB_EINVAL, "null output");
+    *s_out = s_in;
+    if (count == 0) return SHB_OK;
+    if (!d_prob || !d_recs || !d_tile_S) return set_error(SHB_EINVAL, "null buffer");
+    return seq_walk(d_prob, count, (const TileRec *)d_recs, s_in, d_tile_S, s_out, as_stream(stream));
+}
+
+extern "C" int shb_cumsum_find(const double *d_prob, uint64_t count, const double *d_tile_S, double total,
+                               double target, uint64_t *index, void *stream)
+{
+    if (!index) return set_error(SHB_EINVAL, "null output");
+    *index = count;
+    if (count == 0) return SHB_OK;
+    if (!d_prob || !d_tile_S) return set_error(SHB_EINVAL, "null buffer");
+    return search_from_tiles(d_prob, count, d_tile_S, total, target, index, as_stream(stream));
 }

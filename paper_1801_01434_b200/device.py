@@ -251,6 +251,36 @@ def cumsum_search_from(p, s_in: float, target: float) -> int:
     return int(out.value)
 
 
+def cumsum_plan(p, s_hint: float):
+    """Records of the split sequential cumsum (shb_cumsum_records): parallel,
+    from a hint of the running value entering p.  Returns (records, tile_S)."""
+    t = _t()
+    lib = nat.load()
+    nt = int(lib.shb_cumsum_tiles(p.numel()))
+    recs = t.empty(max(nt, 1) * int(lib.shb_cumsum_record_bytes()), dtype=t.uint8, device=p.device)
+    tile_s = t.empty(max(nt, 1), dtype=t.float64, device=p.device)
+    nat.check(lib.shb_cumsum_records(_vp(p), p.numel(), float(s_hint), _vp(recs), _stream()), "cumsum_records")
+    return recs, tile_s
+
+
+def cumsum_walk(p, plan, s_in: float) -> float:
+    """The exact walk from s_in over p (shb_cumsum_walk): the running value after p."""
+    recs, tile_s = plan
+    out = ctypes.c_double(0.0)
+    nat.check(nat.load().shb_cumsum_walk(_vp(p), p.numel(), _vp(recs), float(s_in), _vp(tile_s),
+                                         ctypes.byref(out), _stream()), "cumsum_walk")
+    return float(out.value)
+
+
+def cumsum_find(p, plan, s_out: float, target: float) -> int:
+    """First i whose running value exceeds target, from a walked plan (shb_cumsum_find)."""
+    _, tile_s = plan
+    out = ctypes.c_uint64(0)
+    nat.check(nat.load().shb_cumsum_find(_vp(p), p.numel(), _vp(tile_s), float(s_out), float(target),
+                                         ctypes.byref(out), _stream()), "cumsum_find")
+    return int(out.value)
+
+
 def sample_index(p, u: float) -> tuple[int, float]:
     """searchsorted(cumsum(p), u * cumsum(p)[-1], "right") exactly, and cumsum(p)[-1]."""
     out = ctypes.c_uint64(0)

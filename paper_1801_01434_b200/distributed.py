@@ -8,8 +8,11 @@ exchanges are the ones the algorithm really has:
 1. all_reduce(sum) of the exact class counts  -> every rank draws the same k
 2. all_gather of the per-shard supports       -> every rank holds the comb
 3. all_reduce(sum) of the |V|^2 partial sums  -> the normalisation check
-4. gather of the probability shards to rank 0 -> exact sequential CDF, m
-   broadcast back to every rank
+4. the exact sequential CDF without moving the probabilities: all_gather of
+   the approximate shard sums (hints for every rank's binade records, built
+   in parallel), then the exact running value hops rank to rank (one double
+   per hop), all_gather of the (enter, leave) pairs, and the owning rank's m
+   broadcast back
 
 Every rank replays the same host Sampler stream, so x, k and m agree by
 construction; each output's summation order does not depend on G, so the
@@ -74,11 +77,17 @@ class DeviceOps:
     def sample(self, prob, u):
         return self.dev.sample_index(prob, u)[0]
 
-    def cumsum_total_from(self, prob, s_in):
-        return self.dev.cumsum_total_from(prob, s_in)
+    def approx_sum(self, prob):
+        return self.dev.dsum(prob)
 
-    def cumsum_search_from(self, prob, s_in, target):
-        return self.dev.cumsum_search_from(prob, s_in, target)
+    def cumsum_plan(self, prob, s_hint):
+        return self.dev.cumsum_plan(prob, s_hint)
+
+    def cumsum_walk(self, prob, plan, s_in):
+        return self.dev.cumsum_walk(prob, plan, s_in)
+
+    def cumsum_find(self, prob, plan, s_in, s_out, target):
+        return self.dev.cumsum_find(prob, plan, s_out, target)
 
     def empty(self, n, dtype):
         return self.torch.empty(n, dtype=dtype, device=self.device)
@@ -212,21 +221,31 @@ def _sharded_sample(ops, prob, u: float, q: int, c_lo: int, rank: int, world: in
     probability vector, bit-identical to the single-device read.
 
     np.cumsum is a strictly sequential chain of float64 adds, so the running
-    sum entering shard g is exactly the running sum leaving shard g-1: rank g
-    receives it (one float64), continues the chain over its shard
-    (ops.cumsum_total_from) and sends the result on.  An all_gather of the
-    (enter, leave) pairs gives every rank the total and the shard whose
-    leaving sum first exceeds the target; that rank searches its shard from
-    its entering sum and broadcasts m.  Traffic: O(world) doubles instead of
-    the q-element probability vector."""
+    sum entering shard g is exactly the running sum leaving shard g-1.  Only
+    that carry is serial: every rank first builds its shard's binade records
+    in parallel from a hint of the value entering it (the all-gathered
+    approximate shard sums; exactness never depends on the hint), then the
+    exact carry hops rank to rank through the records-driven walk
+    (ops.cumsum_walk, ~32 tiles of 8192 outputs per warp step).  An
+    all_gather of the (enter, leave) pairs gives every rank the total and the
+    shard whose leaving sum first exceeds the target; that rank searches its
+    walked shard and broadcasts m.  Traffic: O(world) doubles instead of the
+    q-element probability vector."""
     import torch.distributed as dist
     # the scalars travel on the device under NCCL, on the host under gloo
     # (gloo point-to-point takes CPU tensors)
     dev = prob.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    approx = torch.tensor([float(ops.approx_sum(prob))], dtype=torch.float64, device=dev)
+    sums = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(world)]
+    dist.all_gather(sums, approx, group=group)
+    hint = 0.0
+    for g in range(rank):
+        hint += float(sums[g].item())
+    plan = ops.cumsum_plan(prob, hint)
     s_in = torch.zeros(1, dtype=torch.float64, device=dev)
     if rank > 0:
         dist.recv(s_in, src=rank - 1, group=group)
-    s_out = torch.tensor([ops.cumsum_total_from(prob, float(s_in.item()))], dtype=torch.float64, device=dev)
+    s_out = torch.tensor([ops.cumsum_walk(prob, plan, float(s_in.item()))], dtype=torch.float64, device=dev)
     if rank < world - 1:
         dist.send(s_out, dst=rank + 1, group=group)
     pairs = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in range(world)]
@@ -239,7 +258,7 @@ def _sharded_sample(ops, prob, u: float, q: int, c_lo: int, rank: int, world: in
         return q
     mt = torch.zeros(1, dtype=torch.int64, device=dev)
     if rank == owner:
-        mt[0] = c_lo + ops.cumsum_search_from(prob, bounds[owner][0], target)
+        mt[0] = c_lo + ops.cumsum_find(prob, plan, bounds[owner][0], bounds[owner][1], target)
     dist.broadcast(mt, src=owner, group=group)
     return int(mt.item())
 

@@ -68,10 +68,16 @@ class OracleOps:
     def sample(self, prob, u):
         return oracle.sample_index(prob.numpy(), u)
 
-    def cumsum_total_from(self, prob, s_in):
+    def approx_sum(self, prob):
+        return float(prob.sum())
+
+    def cumsum_plan(self, prob, s_hint):
+        return None
+
+    def cumsum_walk(self, prob, plan, s_in):
         return oracle.cumsum_total_from(prob.numpy(), s_in)
 
-    def cumsum_search_from(self, prob, s_in, target):
+    def cumsum_find(self, prob, plan, s_in, s_out, target):
         return oracle.cumsum_search_from(prob.numpy(), s_in, target)
 
     def to_host(self, t):

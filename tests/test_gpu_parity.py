@@ -787,3 +787,42 @@ def test_chained_device_cumsum_matches_whole_vector(golden_dir):
                 got = n if owner is None else cuts[owner] + dev.cumsum_search_from(
                     p[cuts[owner]:cuts[owner + 1]], bounds[owner][0], target)
                 assert got == dev.sample_index(p, u)[0]
+
+
+@pytest.mark.parametrize("hint_kind", ["approx", "zero", "wrong"])
+def test_split_cumsum_records_walk_find(golden_dir, hint_kind):
+    """The split sequential cumsum of the sharded read (distributed._sharded_sample,
+    shb_sample): per-shard records from a hint (the all-gathered approximate
+    shard sums, or a useless 0 / wildly wrong hint), the exact walk chained
+    shard to shard, and the search in the owning shard -- same total (bitwise)
+    and same m as shb_sample_index on the whole vector, whatever the hint."""
+    d = np.load(golden_dir / "sampling.npz")
+    rng = np.random.default_rng(29)
+    ties = np.full(1 << 16, 2.0 ** -20)
+    ties[::3] = 2.0 ** -53
+    zeros = rng.random(1 << 18) * (rng.random(1 << 18) < 0.1)
+    big = rng.random(3 << 20)
+    vecs = [oracle.probabilities(d["state"]), ties, zeros, big / big.sum()]
+    for p_h in vecs:
+        p = torch.from_numpy(np.ascontiguousarray(p_h)).cuda()
+        n = p_h.size
+        for world in (2, 5):
+            cuts = [0] + sorted(rng.choice(np.arange(1, n), world - 1, replace=False).tolist()) + [n]
+            shards = [p[cuts[g]:cuts[g + 1]] for g in range(world)]
+            approx = [dev.dsum(sh) for sh in shards]
+            plans = []
+            for g, sh in enumerate(shards):
+                hint = {"approx": float(sum(approx[:g])), "zero": 0.0, "wrong": 1e6 * (g + 1)}[hint_kind]
+                plans.append(dev.cumsum_plan(sh, hint))
+            bounds, s = [], 0.0
+            for g, sh in enumerate(shards):
+                s_out = dev.cumsum_walk(sh, plans[g], s)
+                bounds.append((s, s_out))
+                s = s_out
+            assert s == dev.sample_index(p, 0.5)[1] == float(np.cumsum(p_h)[-1])
+            for u in list(rng.random(25)) + [0.0, float(np.nextafter(1.0, 0.0))]:
+                target = u * s
+                owner = next((g for g in range(world) if bounds[g][1] > target), None)
+                got = n if owner is None else cuts[owner] + dev.cumsum_find(
+                    shards[owner], plans[owner], bounds[owner][1], target)
+                assert got == dev.sample_index(p, u)[0], (hint_kind, world, u)
