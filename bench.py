@@ -380,6 +380,10 @@ def run_b200(args):
     # every rank runs the _kernels.partial_row_sums seam on its row shard.
     if not args.no_e2e:
         line["e2e"] = e2e_host(args, q, rec, lib, torch, nat, rank, world)
+    # the sharded Born-rule read's pieces, timed on an eighth of this attempt's
+    # probabilities (one rank's shard at N = 8): what an N-GPU step adds
+    if world == 1 and hasattr(rec, "spectrum"):
+        line["multi_gpu_model"] = _cdf_split_model(rec.spectrum[1], q, rec.dft_ms, el_ms / args.steps, torch)
     # FP32 fast path on the same attempt: Horner in FP32 with exact FP64
     # re-seeds every 256 terms; accuracy vs the FP64 spectrum just measured
     if not args.no_fp32 and args.precision == "fp64":
@@ -432,6 +436,42 @@ def run_b200(args):
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def _cdf_split_model(prob, q: int, dft_ms: float, step_ms: float, torch, world: int = 8) -> dict:
+    """Time the split sequential cumsum on one 1/world shard of the spectrum's
+    |V|^2 (device events): records (parallel on every rank) and the exact walk
+    (the only rank-to-rank serial hop), next to the unsplit per-shard scan the
+    round-1 chain serialised.  Model of an N-rank step from these (not a
+    multi-GPU measurement)."""
+    from paper_1801_01434_b200 import device as dev
+    shard = prob[: q // world]
+
+    def timed(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps, out
+
+    hint = 0.0
+    rec_ms, plan = timed(lambda: dev.cumsum_plan(shard, hint))
+    walk_ms, _ = timed(lambda: dev.cumsum_walk(shard, plan, 0.0))
+    old_ms, _ = timed(lambda: dev.cumsum_total_from(shard, 0.0))
+    per_rank_dft = dft_ms / world
+    other = step_ms - dft_ms  # entangle + collapse + sample on one GPU
+    predicted = per_rank_dft + other / world + rec_ms + (world - 1) * walk_ms
+    return {"world": world, "shard_outputs": q // world, "records_ms": rec_ms, "walk_ms_per_hop": walk_ms,
+            "unsplit_scan_ms_per_hop": old_ms, "dft_ms_per_rank": per_rank_dft,
+            "predicted_step_ms": predicted, "predicted_scaling_efficiency": step_ms / world / predicted,
+            "note": "model from single-GPU timings: per-rank DFT = 1/world of this attempt's DFT (outputs split evenly, "
+                    "same per-output work), the other stages split evenly, plus the parallel records and "
+                    "(world - 1) serial carry hops; NCCL collectives (a few scalars and the class counts) not "
+                    "included. No multi-GPU hardware was available to measure it."}
 
 
 # BASELINE.json configs through the public driver, with SURVEY.md 8(d)'s traces:

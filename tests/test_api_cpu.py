@@ -143,3 +143,23 @@ def test_dump_load_roundtrip(tmp_path):
     p.write_bytes(raw[:16 + 32])  # whole complex values, fewer than q
     with pytest.raises(ValueError, match="truncated"):
         qstate.load_state(p)
+
+
+def test_gate_ops_validate_before_the_device():
+    """The gate primitives (qft.py:164-212) check their arguments in the
+    reference's order and with its messages before any device work."""
+    z = np.ones(16, dtype=np.complex128) / 4
+    with pytest.raises(ValueError, match="control and target must differ"):
+        qft.apply_controlled_phase(z, 1, 1, 0.5)
+    with pytest.raises(ValueError, match=r"qubit index 4 out of range for w=4"):
+        qft.apply_controlled_phase(z, 4, 0, 0.5)
+    with pytest.raises(ValueError, match=r"qubit index -1 out of range for w=4"):
+        qft.apply_hadamard(z, -1)
+    with pytest.raises(ValueError, match="size must be a power of two"):
+        qft.apply_hadamard(np.ones(6, dtype=np.complex128), 0)
+    with pytest.raises(ValueError, match="size must be a power of two"):
+        qft.bit_reverse_permute(np.ones(6))
+    with pytest.raises(ValueError, match="circuit engine capped at w <= 12, got w=13"):
+        qft.circuit_qft(np.ones(1 << 13, dtype=np.complex128))
+    with pytest.raises(ValueError, match="circuit engine is gate-level FP64"):
+        qft.transform(z, "circuit", plan=qft.KernelPlan(precision="fp32"))
