@@ -448,6 +448,9 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
             wait_bar(&g_full[gb], (itd >> 1) & 1u);  // tconst[gb] of this tile (built with its G)
             I8_TR(tid == 0 && itd < 64, 2001 + 4 * itd);
             const double2 *sinv = tconst[gb][0] + n0;
+#ifdef SHB_I8_HREG2
+            double2 hreg[OPT];
+#endif
             for (uint64_t sb = 0; sb < p.nsb; sb++, gs++) {
                 const uint32_t ab = (uint32_t)(gs & 1);
                 I8_TR(tid == 0 && gs < 240, 1000 + 4 * gs);
@@ -455,6 +458,27 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 I8_TR(tid == 0 && gs < 240, 1001 + 4 * gs);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t cols = tmem + lane_addr + ab * ACC_COLS + n0;
+#ifdef SHB_I8_HREG2
+                // H in registers; the Re pairs and then the Im pairs (two load round trips)
+                int acc[NPAIR][OPT];
+                double tre[OPT];
+#pragma unroll
+                for (int o = 0; o < NPAIR; o++) ld8(cols + o * NO, acc[o]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int i = 0; i < OPT; i++) tre[i] = combine(acc[0][i], acc[1][i], acc[2][i], acc[3][i]);
+#pragma unroll
+                for (int o = 0; o < NPAIR; o++) ld8(cols + (NPAIR + o) * NO, acc[o]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(&a_empty[ab]);  // the accumulators are in registers
+                I8_TR(tid == 0 && gs < 240, 1002 + 4 * gs);
+#pragma unroll
+                for (int i = 0; i < OPT; i++) {
+                    const double2 tv = make_double2(tre[i], combine(acc[0][i], acc[1][i], acc[2][i], acc[3][i]));
+                    hreg[i] = sb == 0 ? tv : cmad(hreg[i], sinv[i], tv);
+                }
+#else
                 int acc[2 * NPAIR][OPT];
 #pragma unroll
                 for (int o = 0; o < 2 * NPAIR; o++) ld8(cols + o * NO, acc[o]);
@@ -468,7 +492,12 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                                                     combine(acc[4][i], acc[5][i], acc[6][i], acc[7][i]));
                     hrow[i] = sb == 0 ? tv : cmad(hrow[i], sinv[i], tv);
                 }
+#endif
             }
+#ifdef SHB_I8_HREG2
+#pragma unroll
+            for (int i = 0; i < OPT; i++) hrow[i] = hreg[i];
+#endif
             // fold the 128 row-blocks: V' = sum_r w^r H_r as 16 Horner chains of 8
             // row-blocks joined by w^8, in a fixed order for every output
             asm volatile("bar.sync 1, %0;" ::"n"(DRAIN_THREADS) : "memory");
