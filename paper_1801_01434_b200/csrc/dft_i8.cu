@@ -53,8 +53,8 @@
 //    run (g_full / g_empty / c_free);
 //  * warps 0-11 (lane quarter warp % 4, outputs 8 (warp / 4) ...): per
 //    super-block load their accumulators (tcgen05.ld, then the set is
-//    released), combine the digit pairs to FP64 and fold by Horner over
-//    super-blocks, H = H e^{-i phi_SB} + T (H in shared memory); at the tile's
+//    released; Re pairs, then Im pairs), combine the digit pairs to FP64 and
+//    fold by Horner over super-blocks, H = H e^{-i phi_SB} + T; at the tile's
 //    end fold the 128 row-blocks by Horner in w = e^{i phi_32} (8 lanes per
 //    chain, chains joined with w^8), apply the exact seed of the last
 //    super-block, and write V and |V|^2 (hypot^2, as np.abs(.)**2).  Every
@@ -435,7 +435,8 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
     } else {
         // ------------------------------------------------------------ drain + fold
         // thread -> row-block r (TMEM lane) and outputs n0 .. n0 + 7; the Horner
-        // state H[r][n] lives in shared memory (the fold buffer) across super-blocks
+        // state H[r][n] stays in registers across super-blocks and goes to the
+        // fold buffer at the tile's end
         const int quarter = warp & 3, n0 = (warp >> 2) * OPT;
         const int r = 32 * quarter + lane;
         const uint32_t lane_addr = (uint32_t)(32 * quarter) << 16;
@@ -448,9 +449,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
             wait_bar(&g_full[gb], (itd >> 1) & 1u);  // tconst[gb] of this tile (built with its G)
             I8_TR(tid == 0 && itd < 64, 2001 + 4 * itd);
             const double2 *sinv = tconst[gb][0] + n0;
-#ifdef SHB_I8_HREG2
-            double2 hreg[OPT];
-#endif
+            double2 hreg[OPT];  // the Horner state of (row-block r, outputs n0 ..)
             for (uint64_t sb = 0; sb < p.nsb; sb++, gs++) {
                 const uint32_t ab = (uint32_t)(gs & 1);
                 I8_TR(tid == 0 && gs < 240, 1000 + 4 * gs);
@@ -458,7 +457,6 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 I8_TR(tid == 0 && gs < 240, 1001 + 4 * gs);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t cols = tmem + lane_addr + ab * ACC_COLS + n0;
-#ifdef SHB_I8_HREG2
                 // H in registers; the Re pairs and then the Im pairs (two load round trips)
                 int acc[NPAIR][OPT];
                 double tre[OPT];
@@ -478,26 +476,9 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                     const double2 tv = make_double2(tre[i], combine(acc[0][i], acc[1][i], acc[2][i], acc[3][i]));
                     hreg[i] = sb == 0 ? tv : cmad(hreg[i], sinv[i], tv);
                 }
-#else
-                int acc[2 * NPAIR][OPT];
-#pragma unroll
-                for (int o = 0; o < 2 * NPAIR; o++) ld8(cols + o * NO, acc[o]);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(&a_empty[ab]);  // the accumulators are in registers
-                I8_TR(tid == 0 && gs < 240, 1002 + 4 * gs);
-#pragma unroll
-                for (int i = 0; i < OPT; i++) {
-                    const double2 tv = make_double2(combine(acc[0][i], acc[1][i], acc[2][i], acc[3][i]),
-                                                    combine(acc[4][i], acc[5][i], acc[6][i], acc[7][i]));
-                    hrow[i] = sb == 0 ? tv : cmad(hrow[i], sinv[i], tv);
-                }
-#endif
             }
-#ifdef SHB_I8_HREG2
 #pragma unroll
             for (int i = 0; i < OPT; i++) hrow[i] = hreg[i];
-#endif
             // fold the 128 row-blocks: V' = sum_r w^r H_r as 16 Horner chains of 8
             // row-blocks joined by w^8, in a fixed order for every output
             asm volatile("bar.sync 1, %0;" ::"n"(DRAIN_THREADS) : "memory");
