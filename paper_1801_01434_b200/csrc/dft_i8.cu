@@ -105,7 +105,7 @@ constexpr int OPT = NO / (DRAIN_WARPS / 4); // outputs per drain thread: one 8-c
 static_assert(OPT == 8, "tcgen05.ld 32x32b.x8 per (component, pair)");
 constexpr int CHAIN = 8;                  // row-blocks per Horner chain of the tile-end fold
 constexpr int FOLD_CHAINS = LANES / CHAIN;
-static_assert(FOLD_CHAINS * NO == DRAIN_THREADS, "one chain per drain thread");
+static_assert(FOLD_CHAINS * NO == DRAIN_THREADS && FOLD_CHAINS == 16, "one chain per drain thread");
 constexpr double T_SCALE = 0x1p-47;       // units of combine()
 
 __device__ __forceinline__ uint32_t kmajor(int row, int k)
@@ -245,9 +245,10 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
     double2 *fold = reinterpret_cast<double2 *>(smem_raw + 2 * G_BYTES);  // [row-block][NO + 1]
     __shared__ __align__(8) uint64_t g_full[2], g_empty[2], a_full[2], a_empty[2], c_free[2];
     __shared__ uint32_t tmem_base_sh;
-    // per output of a tile (built with its G): e^{-i phi_SB}, w = e^{i phi_32}, w^CHAIN, seed
-    __shared__ double2 tconst[2][4][NO];
+    // per output of a tile (built with its G): e^{-i phi_SB}, w = e^{i phi_32}, w^8, seed, w^32
+    __shared__ double2 tconst[2][5][NO];
     __shared__ double2 rpart[FOLD_CHAINS][NO];
+    __shared__ double2 rquad[FOLD_CHAINS / 4][NO];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint64_t q = p.q, qmask = q - 1;
@@ -362,8 +363,8 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 wait_bar(&c_free[gb], ((it >> 1) - 1) & 1u);   // its drain no longer reads tconst[gb]
             }
             I8_TR(gt == 0 && it < 64, 5001 + 4 * it);
-            static_assert(G_THREADS >= 4 * NO, "one tile constant per G thread");
-            if (gt < 4 * NO) {
+            static_assert(G_THREADS >= 5 * NO, "one tile constant per G thread");
+            if (gt < 5 * NO) {
                 // per-output constants of the tile, exact sincospi of the integer phase
                 const int kind = gt / NO, nn = gt % NO;
                 const uint64_t cc = p.c_begin + t * NO + nn;
@@ -371,12 +372,18 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 const uint64_t idx = kind == 0 ? (uint64_t)SBA * p.stride * cc
                                    : kind == 1 ? (uint64_t)KC * p.stride * cc
                                    : kind == 2 ? (uint64_t)CHAIN * KC * p.stride * cc
-                                               : a_seed * cc;
+                                   : kind == 3 ? a_seed * cc
+                                               : (uint64_t)4 * CHAIN * KC * p.stride * cc;
                 double2 v = phase(idx & qmask, q, p.two_over_q);
                 if (kind == 0) v.y = -v.y;  // e^{-i phi_SB}: Horner runs forward over super-blocks
                 tconst[gb][kind][nn] = v;
             }
+#ifdef SHB_I8_GPROBE
+            // timing probe only (WRONG results): G is built for the first two tiles only
+            if (gt < G_ITEMS && it < 2) {
+#else
             if (gt < G_ITEMS) {
+#endif
                 const int n = gt % NO, ks = gt / NO;  // k-span ks covers k = ks*GSPAN ... + GSPAN - 1
                 const int kc = ks * GSPAN / KC;
                 const uint64_t c = p.c_begin + t * NO + n;
@@ -463,24 +470,36 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
 #pragma unroll
                 for (int o = 0; o < NPAIR; o++) ld8(cols + o * NO, acc[o]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#ifndef SHB_I8_DRAIN_PROBE
 #pragma unroll
                 for (int i = 0; i < OPT; i++) tre[i] = combine(acc[0][i], acc[1][i], acc[2][i], acc[3][i]);
+#else
+#pragma unroll
+                for (int i = 0; i < OPT; i++) tre[i] = 0.0;
+#endif
 #pragma unroll
                 for (int o = 0; o < NPAIR; o++) ld8(cols + (NPAIR + o) * NO, acc[o]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&a_empty[ab]);  // the accumulators are in registers
                 I8_TR(tid == 0 && gs < 240, 1002 + 4 * gs);
+#ifdef SHB_I8_DRAIN_PROBE
+                // timing probe only (WRONG results): no FP64 drain work
+#pragma unroll
+                for (int i = 0; i < OPT; i++) hreg[i].x += (double)(acc[0][i] ^ acc[3][i]);
+#else
 #pragma unroll
                 for (int i = 0; i < OPT; i++) {
                     const double2 tv = make_double2(tre[i], combine(acc[0][i], acc[1][i], acc[2][i], acc[3][i]));
                     hreg[i] = sb == 0 ? tv : cmad(hreg[i], sinv[i], tv);
                 }
+#endif
             }
 #pragma unroll
             for (int i = 0; i < OPT; i++) hrow[i] = hreg[i];
             // fold the 128 row-blocks: V' = sum_r w^r H_r as 16 Horner chains of 8
-            // row-blocks joined by w^8, in a fixed order for every output
+            // row-blocks, joined four at a time by w^8 and the four results by w^32
+            // (a short tree instead of one 16-step chain), in a fixed order
             asm volatile("bar.sync 1, %0;" ::"n"(DRAIN_THREADS) : "memory");
             I8_TR(tid == 0 && itd < 64, 2002 + 4 * itd);
             {
@@ -493,12 +512,22 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 rpart[ch][n] = a;
             }
             asm volatile("bar.sync 1, %0;" ::"n"(DRAIN_THREADS) : "memory");
+            if (tid < FOLD_CHAINS / 4 * NO) {
+                // 4 chains -> 1 by Horner in w^8
+                const int n = tid % NO, g4 = tid / NO;
+                const double2 w8 = tconst[gb][2][n];
+                double2 v = rpart[4 * g4 + 3][n];
+#pragma unroll
+                for (int j = 2; j >= 0; j--) v = cmad(v, w8, rpart[4 * g4 + j][n]);
+                rquad[g4][n] = v;
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(DRAIN_THREADS) : "memory");
             if (tid < NO) {
                 const int n = tid;
-                const double2 wc = tconst[gb][2][n], sd = tconst[gb][3][n];
-                double2 v = rpart[FOLD_CHAINS - 1][n];
+                const double2 w32 = tconst[gb][4][n], sd = tconst[gb][3][n];
+                double2 v = rquad[FOLD_CHAINS / 4 - 1][n];
 #pragma unroll
-                for (int ch = FOLD_CHAINS - 2; ch >= 0; ch--) v = cmad(v, wc, rpart[ch][n]);
+                for (int g4 = FOLD_CHAINS / 4 - 2; g4 >= 0; g4--) v = cmad(v, w32, rquad[g4][n]);
                 const double vr = sd.x * v.x - sd.y * v.y, vi = sd.x * v.y + sd.y * v.x;
                 const uint64_t ci = t * NO + n;
                 if (ci < p.c_count) {
