@@ -111,6 +111,7 @@ struct SeqShared {
     uint64_t P[SEQ_CHUNK];        // inclusive unit prefix of the current range
     uint64_t add[SEQ_CHUNK];      // per-element unit increments
     uint8_t tie[SEQ_CHUNK];
+    uint16_t tlist[SEQ_CHUNK];    // tie positions, ascending (parallel tie resolution)
     double S;                     // exact running sum before `start`
     int start;                    // first unprocessed local index
     int done;
@@ -269,6 +270,52 @@ __global__ void __launch_bounds__(256) tile_rec_kernel(const double *__restrict_
     }
 }
 
+// Resolve ties in index order: a tie rounds half-to-even on the parity of the
+// running unit count just before it, which is the exclusive prefix of the
+// unadjusted increments plus the adjustments of the earlier ties.  One block
+// scan gives every prefix; one thread then visits only the tie positions (a
+// handful per tile) instead of all 8192 elements.  Rare path: kept out of
+// line so it does not raise the register count of the walk.
+__device__ __noinline__ void resolve_ties(SeqShared &sh, uint64_t loc, uint64_t Su)
+{
+    const int tid = threadIdx.x;
+    uint64_t ex = block_excl_sat(loc, sh.warp_tmp);
+    uint64_t nt = 0;
+#pragma unroll 1
+    for (int k = 0; k < SEQ_V; k++) {
+        const int li = tid * SEQ_V + k;
+        sh.P[li] = ex;  // exclusive prefix at li (from `start`)
+        ex = sat_add(ex, sh.add[li]);
+        nt += sh.tie[li];
+    }
+    uint64_t toff = block_excl_sat(nt, sh.warp_tmp);
+#pragma unroll 1
+    for (int k = 0; k < SEQ_V; k++) {
+        const int li = tid * SEQ_V + k;
+        if (sh.tie[li]) sh.tlist[toff++] = (uint16_t)li;
+    }
+    uint64_t ntie = nt;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ntie += __shfl_xor_sync(0xffffffffu, ntie, o);
+    __syncthreads();  // block_excl_sat's last reads of warp_tmp are done
+    if ((tid & 31) == 0) sh.warp_tmp[tid >> 5] = ntie;
+    __syncthreads();
+    if (tid == 0) {
+        uint64_t total_ties = 0;
+        for (int w = 0; w < SEQ_THREADS / 32; w++) total_ties += sh.warp_tmp[w];
+        uint64_t adj = 0;
+        for (uint64_t j = 0; j < total_ties; j++) {
+            const int li = sh.tlist[j];
+            const uint64_t a = sh.add[li];
+            if ((Su + sh.P[li] + adj + a) & 1ull) {  // saturated prefixes lie past a crossing
+                sh.add[li] = a + 1;
+                adj++;
+            }
+        }
+    }
+    __syncthreads();
+}
+
 // Detailed exact walk of one tile by the whole CTA (binade crossings, ties,
 // first nonzero, or the target search).  Updates sh.S / sh.found / sh.done.
 __device__ void walk_tile(const double *__restrict__ p, uint64_t L, uint64_t ck, int mode, double target,
@@ -339,19 +386,7 @@ __device__ void walk_tile(const double *__restrict__ p, uint64_t L, uint64_t ck,
         }
         any_tie = __syncthreads_or(any_tie);
         if (any_tie) {
-            // resolve ties in index order (rare): parity of the running unit count
-            if (tid == 0) {
-                uint64_t run = Su;
-                for (int li = start; li < n; li++) {
-                    uint64_t a = sh.add[li];
-                    if (sh.tie[li] && ((run + a) & 1ull)) {
-                        a += 1;
-                        sh.add[li] = a;
-                    }
-                    run = sat_add(run, a);
-                }
-            }
-            __syncthreads();
+            resolve_ties(sh, loc, Su);
             loc = 0;
 #pragma unroll
             for (int k = 0; k < SEQ_V; k++) loc = sat_add(loc, sh.add[tid * SEQ_V + k]);
