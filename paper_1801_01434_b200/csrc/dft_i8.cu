@@ -91,11 +91,7 @@ constexpr int FOLD_STRIDE = NO + 1;       // complex per row-block row of the fo
 constexpr int FOLD_BYTES = LANES * FOLD_STRIDE * 16;
 constexpr int SMEM_BYTES = 2 * G_BYTES + FOLD_BYTES;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
-#ifndef SHB_I8_GSPAN
-#define SHB_I8_GSPAN 32
-#endif
-constexpr int GSPAN = SHB_I8_GSPAN;        // k per G item (16 or 32)
-static_assert(GSPAN == 16 || GSPAN == 32, "G item span");
+constexpr int GSPAN = 32;                  // k per G item: one K-chunk (16-k items on more warps: slower)
 constexpr int G_ITEMS = NO * BK / GSPAN;   // (output, k-span) items of a tile's G
 constexpr int DRAIN_WARPS = 12, G_WARPS = (G_ITEMS + 31) / 32;
 constexpr int DRAIN_THREADS = DRAIN_WARPS * 32, G_THREADS = G_WARPS * 32;
@@ -378,12 +374,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 if (kind == 0) v.y = -v.y;  // e^{-i phi_SB}: Horner runs forward over super-blocks
                 tconst[gb][kind][nn] = v;
             }
-#ifdef SHB_I8_GPROBE
-            // timing probe only (WRONG results): G is built for the first two tiles only
-            if (gt < G_ITEMS && it < 2) {
-#else
             if (gt < G_ITEMS) {
-#endif
                 const int n = gt % NO, ks = gt / NO;  // k-span ks covers k = ks*GSPAN ... + GSPAN - 1
                 const int kc = ks * GSPAN / KC;
                 const uint64_t c = p.c_begin + t * NO + n;
@@ -470,30 +461,19 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
 #pragma unroll
                 for (int o = 0; o < NPAIR; o++) ld8(cols + o * NO, acc[o]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#ifndef SHB_I8_DRAIN_PROBE
 #pragma unroll
                 for (int i = 0; i < OPT; i++) tre[i] = combine(acc[0][i], acc[1][i], acc[2][i], acc[3][i]);
-#else
-#pragma unroll
-                for (int i = 0; i < OPT; i++) tre[i] = 0.0;
-#endif
 #pragma unroll
                 for (int o = 0; o < NPAIR; o++) ld8(cols + (NPAIR + o) * NO, acc[o]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(&a_empty[ab]);  // the accumulators are in registers
                 I8_TR(tid == 0 && gs < 240, 1002 + 4 * gs);
-#ifdef SHB_I8_DRAIN_PROBE
-                // timing probe only (WRONG results): no FP64 drain work
-#pragma unroll
-                for (int i = 0; i < OPT; i++) hreg[i].x += (double)(acc[0][i] ^ acc[3][i]);
-#else
 #pragma unroll
                 for (int i = 0; i < OPT; i++) {
                     const double2 tv = make_double2(tre[i], combine(acc[0][i], acc[1][i], acc[2][i], acc[3][i]));
                     hreg[i] = sb == 0 ? tv : cmad(hreg[i], sinv[i], tv);
                 }
-#endif
             }
 #pragma unroll
             for (int i = 0; i < OPT; i++) hrow[i] = hreg[i];
