@@ -717,6 +717,13 @@ def _shared_state(q, c0, r, amp, rank, world, torch):
         registered = int(rc) == 0 if not hasattr(rc, "value") else int(rc.value) == 0
     except Exception:
         registered = False
+    if not registered:
+        # a refused registration (e.g. a /dev/shm mapping in a container) leaves a
+        # sticky runtime error that the next library launch check would report
+        try:
+            torch.cuda.cudart().cudaGetLastError()
+        except Exception:
+            pass
     return {"mm": mm, "ptr": ptr, "path": path, "registered": registered}
 
 
@@ -729,6 +736,19 @@ def _e2e_sharded(args, q, M, shared, c_lo, c_hi, lib, torch, nat, rank, world):
         nat.check(lib.shb_partial_row_sums_host(ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(shared["ptr"]),
                                                 None, q, c_lo, c_hi, 0, q), "partial_row_sums_host")
 
+    try:
+        call()
+        ok = 1
+    except RuntimeError:
+        ok = 0  # e.g. several ranks sharing one GPU cannot all use the page-locked mapping
+    flag = torch.tensor([ok], device="cuda")
+    torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+    if not int(flag.item()) and shared["registered"]:
+        try:
+            torch.cuda.cudart().cudaHostUnregister(shared["ptr"])
+        except Exception:
+            pass
+        shared["registered"] = False
     secs = _time_calls(call, 3, world, torch)
     v0 = out.numpy().view(np.complex128)[0] if rank == 0 else complex(0)
     if shared["registered"]:
