@@ -83,6 +83,9 @@ __device__ __forceinline__ void wait_bar(uint64_t *bar, uint32_t ph)
 }
 
 // A: [128][32] bytes (row-major m, k), B: [n][32] bytes (row n, k), D: [128][n] int32
+__device__ int g_load_mode = 0;
+__device__ volatile int g_stop = 0;
+
 template <int MODE, int NACC, int DSTRIDE = 64, int ACOL = 256>
 __global__ void probe(const int8_t *A, const int8_t *B, int n, int b_signed, int a_signed, int reps,
                       int *D, long long *cycles)
@@ -126,6 +129,44 @@ __global__ void probe(const int8_t *A, const int8_t *B, int n, int b_signed, int
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp >= 4) {
+        // background load while warp 0 issues the MMAs
+        double x = threadIdx.x * 1e-3, y = 1.0 + threadIdx.x * 1e-6;
+        double xs[8];
+        float fs[8];
+        uint32_t ks[8];
+        for (int u = 0; u < 8; u++) {
+            xs[u] = x + u;
+            fs[u] = (float)(x + u);
+            ks[u] = threadIdx.x + u;
+        }
+        uint32_t k = threadIdx.x;
+        const long long b0 = clock64();
+        for (int it = 0; it < 4000; it++) {
+            if (g_load_mode == 1) {  // 8 independent DFMA chains (throughput)
+#pragma unroll
+                for (int u = 0; u < 8; u++) xs[u] = fma(xs[u], y, 1e-9);
+            } else if (g_load_mode == 2) {  // ALU
+#pragma unroll
+                for (int u = 0; u < 8; u++) k = (k << 3) ^ (k >> 5) ^ 0x9e37u;
+            } else if (g_load_mode == 3) {  // 8 independent FFMA chains
+#pragma unroll
+                for (int u = 0; u < 8; u++) fs[u] = fmaf(fs[u], 1.0001f, 1e-7f);
+            } else if (g_load_mode == 4) {  // 8 independent IMAD chains
+#pragma unroll
+                for (int u = 0; u < 8; u++) ks[u] = ks[u] * 0x9e3779b1u + 7u;
+            } else if (g_load_mode == 5) {  // 8 independent I2F.F64 + DADD
+#pragma unroll
+                for (int u = 0; u < 8; u++) xs[u] = xs[u] + (double)(int)(ks[u] + it);
+            } else break;
+        }
+        for (int u = 0; u < 8; u++) {
+            x += xs[u] + fs[u];
+            k ^= ks[u];
+        }
+        if (x == 12345.0 || k == 7u) D[0] = 1;
+        if (threadIdx.x == 128) cycles[1] = clock64() - b0;
+    }
     if (warp == 0) {
         const uint64_t bd = sdesc(saddr(sB), 128, sbo), ad = sdesc(saddr(sA), 128, sbo);
         const uint32_t id = idesc(128, n, a_signed, b_signed);
@@ -161,6 +202,7 @@ __global__ void probe(const int8_t *A, const int8_t *B, int n, int b_signed, int
         wait_bar(&bar, 0);
         long long t1 = clock64();
         if (lane == 0) cycles[0] = t1 - t0;
+        if (lane == 0) g_stop = 1;
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -227,14 +269,19 @@ int main()
                    (double)cyc / reps, 128.0 * n / 256);
         }
     };
-    run(probe<0, 1>, "ts", 1);
-    run(probe<0, 2>, "ts", 2);
-    run(probe<0, 4>, "ts", 4);
-    run(probe<0, 4, 24, 392>, "ts d24 a392", 4);
-    run(probe<0, 4, 24, 400>, "ts d24 a400", 4);
-    run(probe<0, 4, 24, 404>, "ts d24 a404", 4);
-    run(probe<1, 1>, "ss", 1);
-    run(probe<1, 2>, "ss", 2);
-    run(probe<1, 4>, "ss", 4);
+    long long *dc2;
+    CK(cudaMalloc(&dc2, 16));
+    for (int lm = 1; lm < 6; lm++)
+        for (int reps : {16, 65536}) {
+            CK(cudaMemcpyToSymbol(g_load_mode, &lm, sizeof(int)));
+            const int n = 24;
+            probe<0, 4><<<1, 512>>>(dA, dB, n, 1, 0, reps, dD, dc2);
+            CK(cudaDeviceSynchronize());
+            long long cyc[2];
+            CK(cudaMemcpy(cyc, dc2, 16, cudaMemcpyDeviceToHost));
+            const char *nm[6] = {"", "DFMA x8 indep", "ALU", "FFMA x8 indep", "IMAD x8 indep", "I2F.F64+DADD x8"};
+            printf("12 warps %-16s x 4000: %8lld cycles (%s MMAs running: %.1f cycles/mma)\n", nm[lm], cyc[1],
+                   reps > 16 ? "with   " : "without", (double)cyc[0] / reps);
+        }
     return 0;
 }
