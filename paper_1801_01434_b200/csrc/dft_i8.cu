@@ -323,17 +323,10 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 const bool last = sb + 1 == p.nsb;
                 const int nch = last ? live_last : KCH, nfull = last ? full_last : KCH;
                 if (elect_one()) {
-#ifdef SHB_I8_MMAPROBE
-                    // timing probe only (WRONG results): MMAs for the first tile only
-                    const int nch_probe = it < 1 ? nch : 0;
-#define SHB_I8_NCH nch_probe
-#else
-#define SHB_I8_NCH nch
-#endif
                     const uint32_t dset = tmem + ab * ACC_COLS;
 #pragma unroll
                     for (int kc = 0; kc < KCH; kc++) {
-                        if (kc < SHB_I8_NCH) {
+                        if (kc < nch) {
                             const uint32_t w128 = tmem + COL_W + (kc < nfull ? 0 : 16), w1 = w128 + 8;
 #pragma unroll
                             for (int o = 0; o < 2 * NPAIR; o++) {
