@@ -158,9 +158,9 @@ __device__ __forceinline__ void wait_bar(uint64_t *bar, uint32_t phase)
             "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(ok)
-            : "r"(smem_addr(bar)), "r"(phase), "r"(0x989680u)
+            : "r"(smem_addr(bar)), "r"(phase), "r"(1000000u)
             : "memory");
-        if (spin > (1u << 24)) asm volatile("trap;");
+        if (spin > (1u << 16)) asm volatile("trap;");  // > ~1 min asleep: a broken pipeline, not a slow one
     }
 }
 
