@@ -271,17 +271,22 @@ int main()
     };
     long long *dc2;
     CK(cudaMalloc(&dc2, 16));
-    for (int lm = 1; lm < 6; lm++)
-        for (int reps : {16, 65536}) {
-            CK(cudaMemcpyToSymbol(g_load_mode, &lm, sizeof(int)));
-            const int n = 24;
-            probe<0, 4><<<1, 512>>>(dA, dB, n, 1, 0, reps, dD, dc2);
-            CK(cudaDeviceSynchronize());
-            long long cyc[2];
-            CK(cudaMemcpy(cyc, dc2, 16, cudaMemcpyDeviceToHost));
-            const char *nm[6] = {"", "DFMA x8 indep", "ALU", "FFMA x8 indep", "IMAD x8 indep", "I2F.F64+DADD x8"};
-            printf("12 warps %-16s x 4000: %8lld cycles (%s MMAs running: %.1f cycles/mma)\n", nm[lm], cyc[1],
-                   reps > 16 ? "with   " : "without", (double)cyc[0] / reps);
-        }
+    for (int mode = 0; mode < 2; mode++)
+        for (int lm = 1; lm < 6; lm++)
+            for (int reps : {16, 65536}) {
+                CK(cudaMemcpyToSymbol(g_load_mode, &lm, sizeof(int)));
+                const int n = 24;
+                if (mode == 0)
+                    probe<0, 4><<<1, 512>>>(dA, dB, n, 1, 0, reps, dD, dc2);
+                else
+                    probe<1, 4><<<1, 512>>>(dA, dB, n, 1, 0, reps, dD, dc2);
+                CK(cudaDeviceSynchronize());
+                long long cyc[2];
+                CK(cudaMemcpy(cyc, dc2, 16, cudaMemcpyDeviceToHost));
+                const char *nm[6] = {"", "DFMA x8 indep", "ALU", "FFMA x8 indep", "IMAD x8 indep", "I2F.F64+DADD x8"};
+                printf("[%s] 12 warps %-16s x 4000: %8lld cycles (%s MMAs running: %.1f cycles/mma)\n",
+                       mode ? "A in smem" : "A in TMEM", nm[lm], cyc[1], reps > 16 ? "with   " : "without",
+                       (double)cyc[0] / reps);
+            }
     return 0;
 }
