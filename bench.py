@@ -554,7 +554,7 @@ def _i8_roofline(rec, q, M, world, dft_s, sms, clk_mhz, kname, ops_per_term, tra
     M128 (row-blocks) x N24 (outputs) x K32 with the weights in TMEM; its
     measured issue floor at N = 24 (15.4 cycles, scripts/i8t_probe.cu) is
     reported beside the tensor peak, and the accumulator drain (FP64
-    combine + Horner, profiles/r02_i8_timeline_q2_30.txt) overlaps it on the
+    combine + Horner, profiles/r02_i8_timeline_q2_30_kch8.txt) overlaps it on the
     second accumulator set."""
     peaks = _measured_peaks()
     bf16 = peaks.get("bf16_tflops")
@@ -563,8 +563,10 @@ def _i8_roofline(rec, q, M, world, dft_s, sms, clk_mhz, kname, ops_per_term, tra
     achieved = ops_per_term * terms / dft_s / 1e12
     # MMA floor of this shape: 15.4 cycles per M128 N24 K32 (524288 int8 ops... 128*24*32 MACs)
     n24_tops = 2 * 128 * 24 * 32 / 15.4 * sms * clk_mhz * 1e6 / 1e12
-    sba = 24576
-    nsb = -(-M // sba)
+    # K-chunks per super-block as csrc/dft_i8.cu picks them: 8 when that needs
+    # fewer super-blocks than 6 (4096 amplitudes per K-chunk)
+    kch = 8 if -(-M // 32768) < -(-M // 24576) else 6
+    nsb = -(-M // (4096 * kch))
     return {"bound": "tensor", "achieved": achieved, "peak": peak_tops, "unit": "TOPS",
             "frac": achieved / peak_tops, "traffic": traffic, "traffic_note": traffic_note,
             "traffic_unit": "bytes/launch", "algorithmic_bytes_per_launch": 24 * (q // world),
@@ -576,7 +578,7 @@ def _i8_roofline(rec, q, M, world, dft_s, sms, clk_mhz, kname, ops_per_term, tra
             "n24_issue_floor": {"tops": n24_tops, "frac": achieved / n24_tops,
                                 "source": "15.4 cycles per M128 N24 K32 kind::i8 MMA with A in TMEM, measured "
                                           "back to back on this B200 (scripts/i8t_probe.cu)"},
-            "superblocks_per_tile": nsb,
+            "superblocks_per_tile": nsb, "kchunks_per_superblock": kch,
             "uniform_comb_only": "the weight operand is the all-ones amplitude matrix of the collapsed register: "
                                  "every row-block's T is the same number, so this throughput is specific to "
                                  "uniform combs (general amplitudes take the DMMA engine)",

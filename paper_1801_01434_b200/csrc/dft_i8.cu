@@ -7,15 +7,16 @@
 //   V_c = scale*amp * sum_j e^{+2 pi i a_j c / q}
 //
 // Index split.  j = sb*SBA + kc*4096 + r*32 + kk: super-block sb (SBA =
-// 24576 amplitudes), K-chunk kc < 6, row-block r < 128 (the MMA's M = the
-// TMEM lanes), kk < 32.  With k = kc*32 + kk (K = 192 per row-block):
+// 4096 KCH amplitudes), K-chunk kc < KCH (6 or 8, Geo below), row-block
+// r < 128 (the MMA's M = the TMEM lanes), kk < 32.  With k = kc*32 + kk
+// (K = 32 KCH per row-block):
 //
 //   V_c = scale*amp * sum_sb sum_r e^{+2 pi i (a0 + sb*SBA*stride + r*32*stride) c / q} T_sb[r, c]
 //   T_sb[r, c] = sum_k A_sb[r, k] * G[k, c],   G[k, c] = e^{+2 pi i (kc*4096 + kk) stride c / q}
 //
 // A_sb[r, k] is the amplitude of a_j (a weight: 1 inside the support, 0
 // past its end); G is the phase matrix of the tile's outputs.  This is a GEMM
-// with M = 128 row-blocks, N = 24 outputs, K = 192.  For the uniform comb A is
+// with M = 128 row-blocks, N = 24 outputs, K = 192 or 256.  For the uniform comb A is
 // all ones, so every row-block's T is the same number: the tensor work is
 // executed as written (and credited), but the throughput is specific to the
 // uniform comb -- a general register would need the amplitudes split into
@@ -26,7 +27,7 @@
 // 8 base-128 digits, X = d0 2^49 + u1 2^42 + ... + u7 (d0 in [-64, 64] s8,
 // u in [0, 127] u8).  Digits pair in one int32 accumulator through the A
 // weights: digit 2p against 128*A (u8), digit 2p+1 against 1*A, so
-// D_p = sum_k A (128 d_2p + d_2p+1), |D_p| < 2^21 for K = 192, and
+// D_p = sum_k A (128 d_2p + d_2p+1), |D_p| < 2^22 for K <= 256, and
 //   2^55 T = D_0 2^42 + D_1 2^28 + D_2 2^14 + D_3     (exact integers).
 // Every product and accumulation in the tensor core is exact.
 //
@@ -42,12 +43,11 @@
 // column (comp*4 + p)*24 + n; [384, 392) weights 128, [392, 400) weights 1,
 // [400, 416) the masked weights of the last super-block's partial K-chunk.
 //
-// Roles (one persistent CTA per SM, 15 warps):
-// Roles (one persistent CTA per SM, 18 warps):
-//  * warp 17 (one elected lane): per super-block 6 x 2 x 4 x 2 = 96 MMAs
+// Roles (one persistent CTA per SM; 18 warps at KCH = 6, 19 at KCH = 8):
+//  * the last warp (one elected lane): per super-block KCH x 2 x 4 x 2 MMAs
 //    (M128 N24 K32, A from TMEM, B = one digit matrix's K-chunk) into the
 //    free accumulator set, committed to a_full[set];
-//  * warps 12-16: build the next tile's 16 digit matrices of G (FP64 phases,
+//  * warps 12-16 (12-17): build the next tile's 16 digit matrices of G (FP64 phases,
 //    exact sincospi every 16 k, FP64 rotation between) and its per-output
 //    constants into the other shared buffer while the current tile's MMAs
 //    run (g_full / g_empty / c_free);
@@ -71,44 +71,59 @@ namespace i8 {
 constexpr int NO = 24;                    // outputs per tile (MMA N)
 constexpr int LANES = 128;                // row-blocks per super-block (MMA M, TMEM lanes)
 constexpr int KC = 32;                    // K per MMA (8-bit operands)
-#ifndef SHB_I8_KCH
-#define SHB_I8_KCH 6
-#endif
-constexpr int KCH = SHB_I8_KCH;           // K-chunks per super-block
-constexpr int BK = KC * KCH;              // K per row-block: columns of G
 constexpr int CHUNK_AMPS = LANES * KC;    // 4096 amplitudes per K-chunk
-constexpr int SBA = CHUNK_AMPS * KCH;     // 16384 amplitudes per super-block
 constexpr int NDIG = 8, NPAIR = 4;
 constexpr int ACC_COLS = 2 * NPAIR * NO;  // one accumulator set
 constexpr int COL_W = 2 * ACC_COLS;       // weights: +0 x128, +8 x1, +16 mask x128, +24 mask x1
 constexpr int TMEM_COLS = 512;
 static_assert(COL_W + 32 <= TMEM_COLS, "TMEM budget");
 constexpr uint32_t LBO = 128;             // next 16-byte k group of a K-major operand
-constexpr uint32_t SBO = (BK / 16) * 128; // next 8-row group
-constexpr int DIG_BYTES = NO * BK;        // one digit matrix (24 x 128 bytes)
-constexpr int G_BYTES = 2 * NDIG * DIG_BYTES;
 constexpr int FOLD_STRIDE = NO + 1;       // complex per row-block row of the fold buffer (bank spread)
 constexpr int FOLD_BYTES = LANES * FOLD_STRIDE * 16;
-constexpr int SMEM_BYTES = 2 * G_BYTES + FOLD_BYTES;
-static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
-constexpr int GSPAN = 32;                  // k per G item: one K-chunk (16-k items on more warps: slower)
-constexpr int G_ITEMS = NO * BK / GSPAN;   // (output, k-span) items of a tile's G
-constexpr int DRAIN_WARPS = 12, G_WARPS = (G_ITEMS + 31) / 32;
-constexpr int DRAIN_THREADS = DRAIN_WARPS * 32, G_THREADS = G_WARPS * 32;
-constexpr int MMA_WARP = DRAIN_WARPS + G_WARPS;
-constexpr int THREADS = (MMA_WARP + 1) * 32;
+constexpr int GSPAN = 32;                 // k per G item: one K-chunk (16-k items on more warps: slower)
+constexpr int DRAIN_WARPS = 12;
+constexpr int DRAIN_THREADS = DRAIN_WARPS * 32;
 constexpr int OPT = NO / (DRAIN_WARPS / 4); // outputs per drain thread: one 8-column TMEM load per accumulator
 static_assert(OPT == 8, "tcgen05.ld 32x32b.x8 per (component, pair)");
 constexpr int CHAIN = 8;                  // row-blocks per Horner chain of the tile-end fold
 constexpr int FOLD_CHAINS = LANES / CHAIN;
 static_assert(FOLD_CHAINS * NO == DRAIN_THREADS && FOLD_CHAINS == 16, "one chain per drain thread");
-constexpr double T_SCALE = 0x1p-47;       // units of combine()
 
+// The geometry that depends on KCH, the K-chunks per super-block (6 or 8,
+// chosen per launch by i8_dft_uniform): K = 32 KCH per row-block, SBA = 4096
+// KCH amplitudes per super-block, a G buffer of 16 digit matrices of 24 x K
+// bytes, one G-builder thread per (output, K-chunk).  The tile-end fold buffer
+// aliases the tile's own G buffer: when the drain reaches the tile end, the
+// tile's last MMAs have completed (it waited for their commit), and the G
+// builders rewrite that buffer only after the drain's c_free for the tile.  So
+// shared memory holds just the two G buffers (KCH = 8: 2 x 96 KB).
+template <int KCH>
+struct Geo {
+    static constexpr int BK = KC * KCH;              // K per row-block: columns of G
+    static constexpr int SBA = CHUNK_AMPS * KCH;     // amplitudes per super-block
+    static constexpr uint32_t SBO = (BK / 16) * 128; // next 8-row group of a K-major operand
+    static constexpr int DIG_BYTES = NO * BK;        // one digit matrix (24 x BK bytes)
+    static constexpr int G_BYTES = 2 * NDIG * DIG_BYTES;
+    static constexpr int SMEM_BYTES = 2 * G_BYTES;
+    static constexpr int G_ITEMS = NO * BK / GSPAN;  // (output, k-span) items of a tile's G
+    static constexpr int G_WARPS = (G_ITEMS + 31) / 32;
+    static constexpr int G_THREADS = G_WARPS * 32;
+    static constexpr int MMA_WARP = DRAIN_WARPS + G_WARPS;
+    static constexpr int THREADS = (MMA_WARP + 1) * 32;
+    static_assert(FOLD_BYTES <= G_BYTES, "the fold buffer fits in a G buffer");
+    static_assert(SMEM_BYTES + 16 * 1024 <= 227 * 1024, "shared memory (dynamic + static)");
+    static_assert(G_THREADS >= 5 * NO, "one tile constant per G thread");
+    // |D_p| <= K (128 * 127 + 127) < 2^22 keeps H = D_1 2^20 + ... below 2^42 (combine)
+    static_assert((int64_t)BK * 16383 < (1LL << 22), "pair accumulators fit combine()");
+};
+
+template <uint32_t SBO>
 __device__ __forceinline__ uint32_t kmajor(int row, int k)
 {
     return (uint32_t)(row >> 3) * SBO + (uint32_t)(k >> 4) * LBO + (uint32_t)(row & 7) * 16u + (uint32_t)(k & 15);
 }
 
+template <uint32_t SBO>
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr)
 {
     return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(LBO >> 4) << 16) | ((uint64_t)(SBO >> 4) << 32) |
@@ -191,6 +206,8 @@ __device__ __forceinline__ double2 phase(uint64_t idx, uint64_t q, double two_ov
     return make_double2(c, s);
 }
 
+constexpr double T_SCALE = 0x1p-47;  // units of combine()
+
 // T in units of 2^-47 from the 4 pair accumulators: 2^47 T = D_0 2^34 + H with
 // H = D_1 2^20 + D_2 2^6 + floor(D_3 / 2^8) < 2^42 (D_1..D_3 >= 0): one
 // IMAD.WIDE.U32 forms the bit pattern of 2^52 + H, one DADD removes the bias
@@ -232,13 +249,17 @@ struct Args {
     } while (0)
 #endif
 
-__global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p)
+template <int KCH>
+__global__ void __launch_bounds__(Geo<KCH>::THREADS, 1) dft_i8_uniform_kernel(const Args p)
 {
+    using GE = Geo<KCH>;
+    constexpr int SBA = GE::SBA, DIG_BYTES = GE::DIG_BYTES, G_BYTES = GE::G_BYTES;
+    constexpr int G_ITEMS = GE::G_ITEMS, G_THREADS = GE::G_THREADS, MMA_WARP = GE::MMA_WARP;
     // no-swizzle K-major operands need 16-byte alignment only; indexing the
     // __shared__ array directly keeps every access in the shared window (LDS/STS)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned char *sG = smem_raw;                                        // [2 buffers][comp][digit] B operands
-    double2 *fold = reinterpret_cast<double2 *>(smem_raw + 2 * G_BYTES);  // [row-block][NO + 1]
+    double2 *const fold0 = reinterpret_cast<double2 *>(smem_raw);  // [row-block][NO + 1] in G buffer 0 (or 1)
     __shared__ __align__(8) uint64_t g_full[2], g_empty[2], a_full[2], a_empty[2], c_free[2];
     __shared__ uint32_t tmem_base_sh;
     // per output of a tile (built with its G): e^{-i phi_SB}, w = e^{i phi_32}, w^8, seed, w^32
@@ -302,7 +323,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
 
     if (warp == MMA_WARP) {
         // ------------------------------------------------------------ MMA issuer
-        const uint64_t gdesc0 = smem_desc(smem_addr(sG));
+        const uint64_t gdesc0 = smem_desc<GE::SBO>(smem_addr(sG));
         const uint32_t id_s = idesc(true), id_u = idesc(false);
         uint64_t gs = 0;  // super-blocks issued so far (accumulator set gs & 1)
         uint32_t it = 0;
@@ -359,7 +380,6 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 wait_bar(&c_free[gb], ((it >> 1) - 1) & 1u);   // its drain no longer reads tconst[gb]
             }
             I8_TR(gt == 0 && it < 64, 5001 + 4 * it);
-            static_assert(G_THREADS >= 5 * NO, "one tile constant per G thread");
             if (gt < 5 * NO) {
                 // per-output constants of the tile, exact sincospi of the integer phase
                 const int kind = gt / NO, nn = gt % NO;
@@ -381,7 +401,7 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                 // G[k, c] = e^{+2 pi i (kc*4096 + kk) stride c / q}, kk < 32: exact sincospi at
                 // kk = 0 and kk = 16, FP64 rotation by e^{+2 pi i stride c / q} in between
                 const double2 w = phase((p.stride * c) & qmask, q, p.two_over_q);
-                unsigned char *buf = sG + gb * G_BYTES + kmajor(n, ks * GSPAN);
+                unsigned char *buf = sG + gb * G_BYTES + kmajor<GE::SBO>(n, ks * GSPAN);
 #pragma unroll 1
                 for (int k16 = 0; k16 < GSPAN / 16; k16++) {
                     const int kk0 = (ks * GSPAN) % KC + 16 * k16;
@@ -438,7 +458,6 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
         const int quarter = warp & 3, n0 = (warp >> 2) * OPT;
         const int r = 32 * quarter + lane;
         const uint32_t lane_addr = (uint32_t)(32 * quarter) << 16;
-        double2 *hrow = fold + r * FOLD_STRIDE + n0;
         uint64_t gs = 0;
         uint32_t itd = 0;
         for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, itd++) {
@@ -475,8 +494,11 @@ __global__ void __launch_bounds__(THREADS, 1) dft_i8_uniform_kernel(const Args p
                     hreg[i] = sb == 0 ? tv : cmad(hreg[i], sinv[i], tv);
                 }
             }
+            // the tile's MMAs are complete (its last commit was awaited): its G buffer
+            // becomes the fold buffer until c_free releases it to the G builders
+            double2 *const fold = fold0 + (size_t)gb * (G_BYTES / sizeof(double2));
 #pragma unroll
-            for (int i = 0; i < OPT; i++) hrow[i] = hreg[i];
+            for (int i = 0; i < OPT; i++) fold[r * FOLD_STRIDE + n0 + i] = hreg[i];
             // fold the 128 row-blocks: V' = sum_r w^r H_r as 16 Horner chains of 8
             // row-blocks, joined four at a time by w^8 and the four results by w^32
             // (a short tree instead of one 16-step chain), in a fixed order
@@ -560,6 +582,17 @@ static unsigned long long *&i8_trace_ptr()
 }
 #endif
 
+template <int KCH>
+static int launch_i8(const i8::Args &a, unsigned grid, cudaStream_t st)
+{
+    using GE = i8::Geo<KCH>;
+    SHB_TRY_CUDA(cudaFuncSetAttribute(i8::dft_i8_uniform_kernel<KCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      GE::SMEM_BYTES));
+    i8::dft_i8_uniform_kernel<KCH><<<grid, GE::THREADS, GE::SMEM_BYTES, st>>>(a);
+    SHB_LAUNCHED();
+    return SHB_OK;
+}
+
 // Caller contract as shb_dft_uniform (validated there); block sums in the
 // caller's shb_dft_num_blocks(c_count, SHB_FP64) layout (slot_outputs per slot).
 int i8_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, uint64_t c_begin, uint64_t c_count,
@@ -577,8 +610,15 @@ int i8_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, ui
     a.c_begin = c_begin;
     a.c_count = c_count;
     a.ntiles = (c_count + NO - 1) / NO;
-    a.nsb = (length + SBA - 1) / SBA;
-    a.last_amps = length - (a.nsb - 1) * SBA;
+    // KCH = 8 when it needs fewer super-blocks than KCH = 6: each super-block
+    // costs one drain pass (the bound of long supports), each K-chunk of a
+    // tile's G one builder item (the bound of short ones) -- profiles/r02_i8_kch_alias.jsonl
+    const uint64_t nsb6 = (length + Geo<6>::SBA - 1) / Geo<6>::SBA;
+    const uint64_t nsb8 = (length + Geo<8>::SBA - 1) / Geo<8>::SBA;
+    const bool k8 = nsb8 < nsb6;
+    const uint64_t sba = k8 ? Geo<8>::SBA : Geo<6>::SBA;
+    a.nsb = k8 ? nsb8 : nsb6;
+    a.last_amps = length - (a.nsb - 1) * sba;
     a.out_re = out_re * T_SCALE;
     a.out_im = out_im * T_SCALE;
     a.out = (double2 *)d_out;
@@ -595,11 +635,8 @@ int i8_dft_uniform(uint64_t length, uint64_t a0, uint64_t stride, uint64_t q, ui
         d_prob = (double *)prob.ptr;
     }
     a.prob = d_prob;
-    SHB_TRY_CUDA(cudaFuncSetAttribute(dft_i8_uniform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      SMEM_BYTES));
     const uint64_t grid = a.ntiles < (uint64_t)sm_count() ? a.ntiles : (uint64_t)sm_count();
-    dft_i8_uniform_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, st>>>(a);
-    SHB_LAUNCHED();
+    SHB_TRY(k8 ? launch_i8<8>(a, (unsigned)grid, st) : launch_i8<6>(a, (unsigned)grid, st));
     if (d_block_sums) {
         const uint64_t nslots = (c_count + slot_outputs - 1) / slot_outputs;
         slot_sums_kernel<<<(unsigned)((nslots + 7) / 8), 256, 0, st>>>(d_prob, c_count, slot_outputs, d_block_sums,

@@ -17,7 +17,7 @@ import torch  # noqa: E402
 from paper_1801_01434_b200 import _native as nat  # noqa: E402
 from paper_1801_01434_b200 import device as dev  # noqa: E402
 
-nat._lib = nat.load(nat.LIB_PATH.parent / "_variants" / "libshorb200_i8_trace.so")
+nat._lib = nat.load(nat.LIB_PATH.parent / "_variants" / os.environ.get("TRACE_LIB", "libshorb200_i8_trace.so"))
 cfg = {"big": (1 << 30, 10943, 16020, 67025), "big2": (1 << 30, 4828, 5340, 201075)}
 q, c0, r, M = next((v for k, v in cfg.items() if k in sys.argv), (1 << 24, 29, 116, 144631))
 for _ in range(2):

@@ -634,10 +634,14 @@ def test_both_fp64_engines_vs_oracle(engine, real_form, monkeypatch):
             assert abs(dev.dsum(brl) - float(prl.sum())) <= 1e-9 * float(prl.sum())
 
 
-@pytest.mark.parametrize("M", [1, 31, 4095, 4096, 4097, 24575, 24576, 24577, 2 * 24576 + 97, 3 * 24576 - 1, 100003])
+# KCH = 6 (24576 per super-block) unless KCH = 8 (32768) needs fewer super-blocks:
+# 24577, 2 * 24576 + 97, 65536, 2 * 32768 + 7 * 4096 + 5 and 100003 run at KCH = 8
+@pytest.mark.parametrize("M", [1, 31, 4095, 4096, 4097, 24575, 24576, 24577, 2 * 24576 + 97, 3 * 24576 - 1, 32768,
+                               65536, 65537, 2 * 32768 + 7 * 4096 + 5, 100003])
 def test_i8_engine_superblock_edges_vs_oracle(M, monkeypatch):
     """The int8 tensor-core FP64 engine around its K-chunk (128 row-blocks x
-    32 = 4096 amplitudes) and super-block (6 chunks = 24576) sizes: full,
+    32 = 4096 amplitudes) and super-block (6 chunks = 24576, or 8 = 32768)
+    sizes: full,
     one-past and ragged last chunks (masked weights in TMEM, dead chunks
     skipped), against the oracle on sampled rows and on an output shard that
     is not a multiple of the 24-output tile, which must also be bitwise
