@@ -92,22 +92,33 @@ __global__ void __launch_bounds__(HIST_THREADS)
     extern __shared__ uint32_t hist[];
     for (uint32_t v = threadIdx.x; v < ncls; v += blockDim.x) hist[v] = 0;
     __syncthreads();
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
-    for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < count; i += stride) {
-        if (i + 4 <= count && ((reinterpret_cast<uintptr_t>(res + i) & 15) == 0)) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(res + i);
-            const uint32_t r4[4] = {v.x, v.y, v.z, v.w};
+    // a CTA covers 16 residues per thread per step: four coalesced 16-byte loads
+    // in flight per thread before its 16 shared atomics (memory-level parallelism)
+    const uint64_t per_cta = (uint64_t)blockDim.x * 16;
+    const bool aligned = (reinterpret_cast<uintptr_t>(res) & 15) == 0;
+    uint64_t base = (uint64_t)blockIdx.x * per_cta;
+    for (; aligned && base + per_cta <= count; base += (uint64_t)gridDim.x * per_cta) {
+        uint4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            v[j] = __ldcs(reinterpret_cast<const uint4 *>(res + base + (uint64_t)j * blockDim.x * 4) + threadIdx.x);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint32_t r4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
             for (int t = 0; t < 4; t++) {
                 if (r4[t] < ncls) atomicAdd(&hist[r4[t]], 1u);
                 else oob = 1;
             }
-        } else {
-            for (uint64_t j = i; j < i + 4 && j < count; j++) {
-                const uint32_t r = res[j];
-                if (r < ncls) atomicAdd(&hist[r], 1u);
-                else oob = 1;
-            }
+        }
+    }
+    // the ragged tail chunk (or every chunk of an unaligned buffer), one residue per thread per step
+    for (; base < count; base += (uint64_t)gridDim.x * per_cta) {
+        const uint64_t hi = base + per_cta < count ? base + per_cta : count;
+        for (uint64_t i = base + threadIdx.x; i < hi; i += blockDim.x) {
+            const uint32_t r = res[i];
+            if (r < ncls) atomicAdd(&hist[r], 1u);
+            else oob = 1;
         }
     }
     if (oob) atomicOr(bad, 1u);
