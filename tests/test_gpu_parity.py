@@ -97,6 +97,23 @@ def test_class_counts_and_compaction(x, n, q):
     assert dev.compact_eq(res_d, n + 5).numel() == 0
 
 
+@pytest.mark.parametrize("lo,hi", [(0, 1), (0, 16383), (0, 16384), (0, 16385), (1, 1 << 20),
+                                   (3, (1 << 22) - 5), (0, 148 * 16384 * 2 + 77)])
+def test_class_counts_ragged_and_unaligned(lo, hi):
+    """The shared-memory histogram's vector path (16 residues per thread per
+    step, 16-byte loads) and its scalar tail: sizes around one CTA step
+    (1024 x 16), several grid strides, and buffers that start off the 16-byte
+    alignment (a shard view res[lo:]) -- all exact against the oracle."""
+    x, n, q = 1991, 3127, 1 << 22
+    full = dev.modexp(x, n, q)
+    hi = min(hi, q)
+    res = oracle.modexp_residues(x, n, q)[lo:hi]
+    counts = dev.class_counts(full[lo:hi], n).cpu().numpy()
+    assert np.array_equal(counts.astype(np.uint64), oracle.class_counts(res, n))
+    with pytest.raises(ValueError):
+        dev.class_counts(full[lo:hi], int(res.max()))  # a residue >= ncls is an error, not a silent drop
+
+
 def test_measure_sweep_vs_reference(kats):
     rows = kats["measure_sweep"]
     for row in rows:
