@@ -113,8 +113,8 @@ struct Geo {
     static_assert(FOLD_BYTES <= G_BYTES, "the fold buffer fits in a G buffer");
     static_assert(SMEM_BYTES + 16 * 1024 <= 227 * 1024, "shared memory (dynamic + static)");
     static_assert(G_THREADS >= 5 * NO, "one tile constant per G thread");
-    // |D_p| <= K (128 * 127 + 127) < 2^22 keeps H = D_1 2^20 + ... below 2^42 (combine)
-    static_assert((int64_t)BK * 16383 < (1LL << 22), "pair accumulators fit combine()");
+    // |D_p| <= K (128 * 127 + 127) < 2^22 keeps L = D_1 2^20 + ... below 2^42 (combine_add)
+    static_assert((int64_t)BK * 16383 < (1LL << 22), "pair accumulators fit combine_add()");
 };
 
 template <uint32_t SBO>
@@ -206,21 +206,27 @@ __device__ __forceinline__ double2 phase(uint64_t idx, uint64_t q, double two_ov
     return make_double2(c, s);
 }
 
-constexpr double T_SCALE = 0x1p-47;  // units of combine()
+constexpr double T_SCALE = 0x1p-47;  // units of combine_add()
 
-// T in units of 2^-47 from the 4 pair accumulators: 2^47 T = D_0 2^34 + H with
-// H = D_1 2^20 + D_2 2^6 + floor(D_3 / 2^8) < 2^42 (D_1..D_3 >= 0): one
-// IMAD.WIDE.U32 forms the bit pattern of 2^52 + H, one DADD removes the bias
-// (exact), D_0 (signed) through one I2F, one DFMA (the only rounding; the
-// dropped bits of D_3 are <= 2^-47 absolute on T).
-__device__ __forceinline__ double combine(int d0, int d1, int d2, int d3)
+// H + T in units of 2^-47 from the 4 pair accumulators and the running sum a:
+// 2^47 T = D_0 2^34 + L with L = D_1 2^20 + D_2 2^6 + floor(D_3 / 2^8) < 2^42
+// (D_1..D_3 >= 0).  One IMAD.WIDE.U32 forms the bit pattern of 2^52 + L; the
+// bias goes into the signed digit, (D_0 - 2^18) 2^34 = D_0 2^34 - 2^52, so one
+// I2F, one DADD (2^52 + L + a) and one DFMA give a + 2^47 T with two
+// roundings (the dropped bits of D_3 are <= 2^-47 absolute on T).
+__device__ __forceinline__ double combine_add(int d0, int d1, int d2, int d3, double a)
 {
     const uint32_t l = ((uint32_t)d2 << 6) + ((uint32_t)d3 >> 8);
     unsigned long long hb;
     asm("{\n\t.reg .b64 a;\n\tmov.b64 a, {%1, %2};\n\tmad.wide.u32 %0, %3, 1048576, a;\n\t}"
         : "=l"(hb)
         : "r"(l), "r"(0x43300000u), "r"((uint32_t)d1));
-    return fma((double)d0, 0x1p34, __longlong_as_double((long long)hb) - 0x1p52);
+    return fma((double)(d0 - (1 << 18)), 0x1p34, __longlong_as_double((long long)hb) + a);
+}
+
+__device__ __forceinline__ double2 rot(double2 g, double2 w)  // g*w
+{
+    return make_double2(fma(g.x, w.x, -g.y * w.y), fma(g.x, w.y, g.y * w.x));
 }
 
 __device__ __forceinline__ double2 cmad(double2 h, double2 w, double2 t)  // h*w + t
@@ -466,7 +472,15 @@ __global__ void __launch_bounds__(Geo<KCH>::THREADS, 1) dft_i8_uniform_kernel(co
             wait_bar(&g_full[gb], (itd >> 1) & 1u);  // tconst[gb] of this tile (built with its G)
             I8_TR(tid == 0 && itd < 64, 2001 + 4 * itd);
             const double2 *sinv = tconst[gb][0] + n0;
-            double2 hreg[OPT];  // the Horner state of (row-block r, outputs n0 ..)
+            // the Horner state of (row-block r, outputs n0 ..), kept pre-rotated: after
+            // super-block sb it holds H_sb e^{-i phi_SB}, so the next super-block's
+            // update H = hreg + T folds into the accumulator combine (a DADD and a
+            // DFMA per component after the loads) and the rotation's FP64 latency
+            // overlaps the next a_full wait and TMEM loads instead of following them
+            // (3 % faster at seed 2 than H = H e^{-i phi_SB} + T after the loads)
+            double2 hreg[OPT];
+#pragma unroll
+            for (int i = 0; i < OPT; i++) hreg[i] = make_double2(0.0, 0.0);
             for (uint64_t sb = 0; sb < p.nsb; sb++, gs++) {
                 const uint32_t ab = (uint32_t)(gs & 1);
                 I8_TR(tid == 0 && gs < 240, 1000 + 4 * gs);
@@ -481,7 +495,7 @@ __global__ void __launch_bounds__(Geo<KCH>::THREADS, 1) dft_i8_uniform_kernel(co
                 for (int o = 0; o < NPAIR; o++) ld8(cols + o * NO, acc[o]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int i = 0; i < OPT; i++) tre[i] = combine(acc[0][i], acc[1][i], acc[2][i], acc[3][i]);
+                for (int i = 0; i < OPT; i++) tre[i] = combine_add(acc[0][i], acc[1][i], acc[2][i], acc[3][i], hreg[i].x);
 #pragma unroll
                 for (int o = 0; o < NPAIR; o++) ld8(cols + (NPAIR + o) * NO, acc[o]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -490,8 +504,9 @@ __global__ void __launch_bounds__(Geo<KCH>::THREADS, 1) dft_i8_uniform_kernel(co
                 I8_TR(tid == 0 && gs < 240, 1002 + 4 * gs);
 #pragma unroll
                 for (int i = 0; i < OPT; i++) {
-                    const double2 tv = make_double2(tre[i], combine(acc[0][i], acc[1][i], acc[2][i], acc[3][i]));
-                    hreg[i] = sb == 0 ? tv : cmad(hreg[i], sinv[i], tv);
+                    const double2 hv =
+                        make_double2(tre[i], combine_add(acc[0][i], acc[1][i], acc[2][i], acc[3][i], hreg[i].y));
+                    hreg[i] = sb + 1 < p.nsb ? rot(hv, sinv[i]) : hv;
                 }
             }
             // the tile's MMAs are complete (its last commit was awaited): its G buffer
