@@ -239,7 +239,10 @@ int shb_cumsum_find(const double *d_prob, uint64_t count, const double *d_tile_S
  * the C-level equivalents of the reference calls, for FFI users.
  */
 /* qft.dense_dft (tiles == 1) / qft.tiled_dft (tiles >= 2) on a host
- * complex128[q] state -> host complex128[q] output, scaled by 1/sqrt(q). */
+ * complex128[q] state -> host complex128[q] output, scaled by 1/sqrt(q).
+ * Both copies overlap the DFT (output slices; a speculative start from the
+ * state's head when it holds a uniform progression, confirmed by a scan of
+ * the whole state).  Page-locked host buffers make the overlap real. */
 int shb_dense_dft_host(const double *state, uint64_t q, uint32_t tiles,
                        int precision, double *out);
 

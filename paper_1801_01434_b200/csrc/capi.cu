@@ -385,46 +385,53 @@ int shb_host_measure_class(const uint64_t *counts, uint64_t ncls, uint64_t q, do
 // the _kernels.partial_row_sums seam.  Device memory is stream-ordered and
 // freed before return.
 
+// The state's progression descriptor and kernel choice (what the DFT launch needs).
+struct ProgKind {
+    uint64_t a0 = 0, stride = 1, len = 0;
+    int uni = 0, real = 0;
+    double ur = 0.0, ui = 0.0;
+};
+
+static int scan_progression(const double *d_state, uint64_t n, Scratch &d_amps, ProgKind &k, cudaStream_t s)
+{
+    SHB_TRY(shb_state_progression(d_state, n, &k.a0, &k.stride, &k.len, s));
+    SHB_TRY(scratch_alloc(d_amps, (k.len ? k.len : 1) * 16, s));
+    if (k.len) SHB_TRY(shb_gather_progression(d_state, k.a0, k.stride, k.len, (double *)d_amps.ptr, s));
+    if (k.len) SHB_TRY(shb_progression_kind((const double *)d_amps.ptr, k.len, &k.uni, &k.real, &k.ur, &k.ui, s));
+    return SHB_OK;
+}
+
 static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t index_base,
                            uint64_t q, uint64_t c_begin, uint64_t c_count, uint32_t tiles,
                            double scale, int precision, double *out_host)
 {
-    cudaStream_t st = nullptr, cp = nullptr;
-    SHB_TRY_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     struct StreamGuard {
-        cudaStream_t s;
+        cudaStream_t s = nullptr;
         ~StreamGuard() {
             if (s) cudaStreamDestroy(s);
         }
-    } guard{st};
-    SHB_TRY_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
-    StreamGuard cp_guard{cp};
+    } st_g, cp_g, up_g;
+    SHB_TRY_CUDA(cudaStreamCreateWithFlags(&st_g.s, cudaStreamNonBlocking));  // DFT
+    SHB_TRY_CUDA(cudaStreamCreateWithFlags(&cp_g.s, cudaStreamNonBlocking));  // D2H of output slices
+    SHB_TRY_CUDA(cudaStreamCreateWithFlags(&up_g.s, cudaStreamNonBlocking));  // bulk H2D + full scan
+    cudaStream_t st = st_g.s, cp = cp_g.s, up = up_g.s;
     int rc = SHB_OK;
     {
-        Scratch d_state, d_amps, d_out;
+        Scratch d_state, d_amps, d_head_amps, d_out;
         // declared after the buffers, so destroyed before them on EVERY exit
-        // path: the stream-ordered frees (on st) are enqueued only once both
-        // streams -- including a D2H copy still reading d_out on cp -- drained
+        // path: the stream-ordered frees (on st) are enqueued only once every
+        // stream -- including a D2H copy still reading d_out on cp -- drained
         struct DrainGuard {
-            cudaStream_t a, b;
+            cudaStream_t a, b, c;
             ~DrainGuard() {
                 cudaStreamSynchronize(a);
                 cudaStreamSynchronize(b);
+                cudaStreamSynchronize(c);
             }
-        } drain{cp, st};
+        } drain{cp, up, st};
         SHB_TRY(scratch_alloc(d_state, nstate * 16, st));
-        SHB_TRY_CUDA(cudaMemcpyAsync(d_state.ptr, state_host, nstate * 16, cudaMemcpyHostToDevice, st));
-        uint64_t a0 = 0, stride = 1, len = 0;
-        SHB_TRY(shb_state_progression((const double *)d_state.ptr, nstate, &a0, &stride, &len, st));
-        SHB_TRY(scratch_alloc(d_amps, (len ? len : 1) * 16, st));
-        if (len) SHB_TRY(shb_gather_progression((const double *)d_state.ptr, a0, stride, len,
-                                                (double *)d_amps.ptr, st));
         SHB_TRY(scratch_alloc(d_out, c_count * 16, st));
-        // data-selected kernel: a uniform comb (e.g. a collapsed register) takes the
-        // constant-operand path, anything else the TMA-staged amplitude stream
-        int uni = 0, real = 0;
-        double ur = 0.0, ui = 0.0;
-        if (len) SHB_TRY(shb_progression_kind((const double *)d_amps.ptr, len, &uni, &real, &ur, &ui, st));
+        SHB_TRY_CUDA(cudaStreamSynchronize(st));  // the allocations are visible to every stream
         // output slices: slice i's D2H copy (second stream) overlaps slice i+1's
         // DFT when out_host is page-locked (pageable memory serialises the copy).
         // Outputs are independent sums, so slicing changes no value.
@@ -440,21 +447,56 @@ static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t i
         } ev_guard{ev, &nev};
         for (; nev < nslice; nev++) SHB_TRY_CUDA(cudaEventCreateWithFlags(&ev[nev], cudaEventDisableTiming));
         double *dout = (double *)d_out.ptr;
-        for (int i = 0; i < nslice && rc == SHB_OK; i++) {
+        auto launch_slice = [&](int i, const ProgKind &k, const double *amps) -> int {
             const uint64_t lo = c_count * i / nslice, hi = c_count * (i + 1) / nslice;
-            if (uni)
-                rc = shb_dft_uniform(ur, ui, len, a0 + index_base, stride, q, c_begin + lo, hi - lo, tiles,
-                                     scale, precision, dout + 2 * lo, nullptr, nullptr, st);
-            else
-                rc = (real ? shb_dft_real : shb_dft)((const double *)d_amps.ptr, len, a0 + index_base, stride, q,
-                                                     c_begin + lo, hi - lo, tiles, scale, precision, dout + 2 * lo,
-                                                     nullptr, nullptr, st);
-            if (rc != SHB_OK) break;
+            int r = k.uni ? shb_dft_uniform(k.ur, k.ui, k.len, k.a0 + index_base, k.stride, q, c_begin + lo, hi - lo,
+                                            tiles, scale, precision, dout + 2 * lo, nullptr, nullptr, st)
+                          : (k.real ? shb_dft_real : shb_dft)(amps, k.len, k.a0 + index_base, k.stride, q,
+                                                              c_begin + lo, hi - lo, tiles, scale, precision,
+                                                              dout + 2 * lo, nullptr, nullptr, st);
+            if (r != SHB_OK) return r;
             SHB_TRY_CUDA(cudaEventRecord(ev[i], st));
             SHB_TRY_CUDA(cudaStreamWaitEvent(cp, ev[i], 0));
-            SHB_TRY_CUDA(cudaMemcpyAsync(out_host + 2 * lo, dout + 2 * lo, (hi - lo) * 16, cudaMemcpyDeviceToHost,
-                                         cp));
+            SHB_TRY_CUDA(cudaMemcpyAsync(out_host + 2 * lo, dout + 2 * lo, (hi - lo) * 16, cudaMemcpyDeviceToHost, cp));
+            return SHB_OK;
+        };
+
+        // Speculative start.  A large state is uploaded as a head (1/64) and
+        // the rest; if the head holds a uniform progression, the DFT of the
+        // first output slice starts at once, assuming the progression runs to
+        // the end of the state (a full comb, as a collapsed register is),
+        // while the rest uploads and the whole state is scanned on `up`.  The
+        // scan then decides: the same descriptor -> the speculative slice is
+        // exactly the slice the plain path computes and the others follow;
+        // anything else -> the plain path (the speculative slice is redone).
+        const uint64_t head = nslice > 1 && nstate >= (1ull << 24) ? nstate / 64 : nstate;
+        ProgKind spec;
+        bool speculating = false;
+        SHB_TRY_CUDA(cudaMemcpyAsync(d_state.ptr, state_host, head * 16, cudaMemcpyHostToDevice, st));
+        if (head < nstate) {
+            SHB_TRY_CUDA(cudaMemcpyAsync((double *)d_state.ptr + 2 * head, state_host + 2 * head,
+                                         (nstate - head) * 16, cudaMemcpyHostToDevice, up));
+            ProgKind h;
+            SHB_TRY(scan_progression((const double *)d_state.ptr, head, d_head_amps, h, st));
+            if (h.uni && h.len >= 2) {
+                spec = h;
+                spec.len = (nstate - 1 - h.a0) / h.stride + 1;
+                speculating = true;
+                SHB_TRY(launch_slice(0, spec, nullptr));
+            }
         }
+        // the whole-state scan: on `up` behind the bulk upload (the head's copy on
+        // st is complete -- its scan synchronised st), on st when there is no split
+        ProgKind k;
+        SHB_TRY(scan_progression((const double *)d_state.ptr, nstate, d_amps, k, head < nstate ? up : st));
+        const bool confirmed = speculating && k.uni && k.a0 == spec.a0 && k.stride == spec.stride &&
+                               k.len == spec.len && k.ur == spec.ur && k.ui == spec.ui;
+        if (speculating && !confirmed) {
+            // the slice-0 copy may have read a wrong spectrum: it is overwritten below
+            SHB_TRY_CUDA(cudaStreamSynchronize(cp));
+        }
+        for (int i = confirmed ? 1 : 0; i < nslice && rc == SHB_OK; i++)
+            rc = launch_slice(i, k, (const double *)d_amps.ptr);
         SHB_TRY_CUDA(cudaStreamSynchronize(cp));
         SHB_TRY_CUDA(cudaStreamSynchronize(st));
         if (rc != SHB_OK) return rc;

@@ -314,6 +314,39 @@ def test_host_abi_dropins(golden_dir):
         nat.check(lib.shb_dense_dft_host(z.ctypes.data, 1000, 1, 0, out.ctypes.data))
 
 
+@pytest.mark.parametrize("kind", ["full_comb", "partial_comb", "late_bump", "random_head"])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_dense_dft_speculative_start(kind, pinned):
+    """shb_dense_dft_host on a 2^24 state starts the first output slice's DFT
+    from the uploaded head (1/64) when the head is a uniform progression,
+    assuming a full comb, and confirms with a scan of the whole state.  Every
+    outcome -- confirmed (full comb), refuted by the length (partial comb) or
+    by the amplitudes (a bump past the head), or no speculation (non-uniform
+    head) -- must give exactly the bits of the plain device path
+    (qft.dense_dft), in pageable and in page-locked host memory."""
+    q, c0, r = 1 << 24, 29, 116
+    rng = np.random.default_rng(3)
+    M = (q - 1 - c0) // r + 1
+    st = torch.zeros(2 * q, dtype=torch.float64, pin_memory=pinned).numpy().view(np.complex128)
+    idx = c0 + r * np.arange(M)
+    st[idx] = 1 / math.sqrt(M)
+    if kind == "partial_comb":
+        st[idx[M // 2:]] = 0
+    elif kind == "late_bump":
+        st[idx[3 * M // 4]] *= 2
+    elif kind == "random_head":
+        st[idx[:100]] = rng.standard_normal(100)
+    out = torch.empty(2 * q, dtype=torch.float64, pin_memory=pinned).numpy().view(np.complex128)
+    lib = nat.load()
+    nat.check(lib.shb_dense_dft_host(st.ctypes.data, q, 1, 0, out.ctypes.data))
+    ref = np.asarray(qft.dense_dft(st, qft.build_twiddles(q, max_width=24), qft.KernelPlan()))
+    assert np.array_equal(out.view(np.uint64), ref.view(np.uint64))
+    rows = rng.integers(0, q, 64, dtype=np.uint64)
+    supp = np.flatnonzero(st).astype(np.uint64)
+    want = oracle.dft_rows(supp, st[supp.astype(np.int64)], q, rows)
+    assert np.max(np.abs(out[rows.astype(np.int64)] - want)) < 1e-12 * max(1.0, np.abs(want).max())
+
+
 # ------------------------------------------------------------------ sampling
 
 def _adversarial_probs(rng, n):
