@@ -447,6 +447,9 @@ static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t i
         } ev_guard{ev, &nev};
         for (; nev < nslice; nev++) SHB_TRY_CUDA(cudaEventCreateWithFlags(&ev[nev], cudaEventDisableTiming));
         double *dout = (double *)d_out.ptr;
+        // every slice's DFT is enqueued before any D2H copy is issued: a copy to
+        // pageable memory blocks the host until it is done, and the DFTs of the
+        // later slices must already be queued behind it
         auto launch_slice = [&](int i, const ProgKind &k, const double *amps) -> int {
             const uint64_t lo = c_count * i / nslice, hi = c_count * (i + 1) / nslice;
             int r = k.uni ? shb_dft_uniform(k.ur, k.ui, k.len, k.a0 + index_base, k.stride, q, c_begin + lo, hi - lo,
@@ -456,6 +459,10 @@ static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t i
                                                               dout + 2 * lo, nullptr, nullptr, st);
             if (r != SHB_OK) return r;
             SHB_TRY_CUDA(cudaEventRecord(ev[i], st));
+            return SHB_OK;
+        };
+        auto copy_slice = [&](int i) -> int {
+            const uint64_t lo = c_count * i / nslice, hi = c_count * (i + 1) / nslice;
             SHB_TRY_CUDA(cudaStreamWaitEvent(cp, ev[i], 0));
             SHB_TRY_CUDA(cudaMemcpyAsync(out_host + 2 * lo, dout + 2 * lo, (hi - lo) * 16, cudaMemcpyDeviceToHost, cp));
             return SHB_OK;
@@ -491,12 +498,10 @@ static int dft_host_common(const double *state_host, uint64_t nstate, uint64_t i
         SHB_TRY(scan_progression((const double *)d_state.ptr, nstate, d_amps, k, head < nstate ? up : st));
         const bool confirmed = speculating && k.uni && k.a0 == spec.a0 && k.stride == spec.stride &&
                                k.len == spec.len && k.ur == spec.ur && k.ui == spec.ui;
-        if (speculating && !confirmed) {
-            // the slice-0 copy may have read a wrong spectrum: it is overwritten below
-            SHB_TRY_CUDA(cudaStreamSynchronize(cp));
-        }
+        // refuted: slice 0 is recomputed (stream order on st) before its copy
         for (int i = confirmed ? 1 : 0; i < nslice && rc == SHB_OK; i++)
             rc = launch_slice(i, k, (const double *)d_amps.ptr);
+        for (int i = 0; i < nslice && rc == SHB_OK; i++) rc = copy_slice(i);
         SHB_TRY_CUDA(cudaStreamSynchronize(cp));
         SHB_TRY_CUDA(cudaStreamSynchronize(st));
         if (rc != SHB_OK) return rc;

@@ -142,6 +142,18 @@ def _support_of(state, q: int):
 
 
 def _run(state, q: int, tiles: int, precision: str):
+    if not isinstance(state, (dev.DeviceVector, dev.CollapsedAmplitudes, dev.UniformAmplitudes)):
+        # host in, host out: the C-ABI drop-in overlaps both copies with the DFT
+        # (capi.cu dft_host_common) and picks the same kernel from the same data
+        arr = np.ascontiguousarray(state, dtype=np.complex128)
+        if arr.shape != (q,):
+            raise ValueError(f"state length {arr.shape} does not match q={q}")
+        nat.require_cuda()
+        lib = nat.load()
+        out = np.empty(q, dtype=np.complex128)
+        nat.check(lib.shb_dense_dft_host(arr.ctypes.data, q, tiles, dev.PRECISIONS[precision], out.ctypes.data),
+                  "dense_dft")
+        return out
     amps, length, a0, stride, host, real = _support_of(state, q)
     if isinstance(amps, complex):
         out, prob, bsum = dev.dft_uniform(amps, length, a0, stride, q, 0, q, tiles=tiles,

@@ -322,8 +322,9 @@ def test_host_dense_dft_speculative_start(kind, pinned):
     assuming a full comb, and confirms with a scan of the whole state.  Every
     outcome -- confirmed (full comb), refuted by the length (partial comb) or
     by the amplitudes (a bump past the head), or no speculation (non-uniform
-    head) -- must give exactly the bits of the plain device path
-    (qft.dense_dft), in pageable and in page-locked host memory."""
+    head) -- must give exactly the bits of the device-resident path
+    (qft.dense_dft on a DeviceSpectrum), in pageable and in page-locked host
+    memory."""
     q, c0, r = 1 << 24, 29, 116
     rng = np.random.default_rng(3)
     M = (q - 1 - c0) // r + 1
@@ -339,7 +340,8 @@ def test_host_dense_dft_speculative_start(kind, pinned):
     out = torch.empty(2 * q, dtype=torch.float64, pin_memory=pinned).numpy().view(np.complex128)
     lib = nat.load()
     nat.check(lib.shb_dense_dft_host(st.ctypes.data, q, 1, 0, out.ctypes.data))
-    ref = np.asarray(qft.dense_dft(st, qft.build_twiddles(q, max_width=24), qft.KernelPlan()))
+    on_dev = dev.DeviceSpectrum(q, torch.from_numpy(st.view(np.float64)).cuda())
+    ref = qft.dense_dft(on_dev, qft.build_twiddles(q, max_width=24), qft.KernelPlan()).numpy()
     assert np.array_equal(out.view(np.uint64), ref.view(np.uint64))
     rows = rng.integers(0, q, 64, dtype=np.uint64)
     supp = np.flatnonzero(st).astype(np.uint64)
