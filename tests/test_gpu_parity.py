@@ -349,6 +349,24 @@ def test_host_dense_dft_speculative_start(kind, pinned):
     assert np.max(np.abs(out[rows.astype(np.int64)] - want)) < 1e-12 * max(1.0, np.abs(want).max())
 
 
+@pytest.mark.parametrize("tiles,precision", [(4, "fp64"), (1, "fp32"), (2, "fp32")])
+def test_host_dense_dft_speculative_tiles_and_fp32(tiles, precision):
+    """The speculative start with the split-K (tiled_dft) and FP32 fast-path
+    kernels: the host-buffer call equals the device-resident path bit for bit."""
+    q, c0, r = 1 << 24, 5, 300
+    M = (q - 1 - c0) // r + 1
+    st = np.zeros(q, dtype=np.complex128)
+    st[c0 + r * np.arange(M)] = 1 / math.sqrt(M)
+    out = np.empty(q, dtype=np.complex128)
+    lib = nat.load()
+    nat.check(lib.shb_dense_dft_host(st.ctypes.data, q, tiles, dev.PRECISIONS[precision], out.ctypes.data))
+    on_dev = dev.DeviceSpectrum(q, torch.from_numpy(st.view(np.float64)).cuda())
+    plan = qft.KernelPlan(tiles=tiles, precision=precision)
+    fn = qft.tiled_dft if tiles > 1 else qft.dense_dft
+    ref = fn(on_dev, qft.build_twiddles(q, max_width=24), plan).numpy()
+    assert np.array_equal(out.view(np.uint64), ref.view(np.uint64))
+
+
 # ------------------------------------------------------------------ sampling
 
 def _adversarial_probs(rng, n):
