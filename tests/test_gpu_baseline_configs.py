@@ -1,6 +1,6 @@
 """GPU parity at BASELINE.json's two largest configs, through the public driver.
 
-``shor.run_shor`` runs n = 32399 at q = 2^30 (Sampler seeds 8, 2, 0) and
+``shor.run_shor`` runs n = 32399 at q = 2^30 (Sampler seeds 8, 2, 3, 0) and
 n = 46927 at q = 2^32 (seed 0) end to end on the device.  Every attempt's
 trace (x, k, c0, r, M, m, outcome kind, factors) is asserted against
 SURVEY.md 8(d)'s table (reference: shor.py:136-201, qstate.py:86-114).
@@ -46,6 +46,8 @@ from paper_1801_01434_b200 import qft, shor  # noqa: E402
 TRACES = {
     (32399, 8): ([(10594, 31897, 10943, 16020, 67025, 342163047, "factors")], [179, 181]),
     (32399, 2): ([(8477, 9557, 4828, 5340, 201075, 874074104, "factors")], [179, 181]),
+    # SURVEY 8(d)'s alternative north-star seed (M = 335125: 10.2 super-blocks at KCH = 8)
+    (32399, 3): ([(2776, 7537, 3118, 3204, 335125, 860266936, "factors")], [179, 181]),
     (32399, 0): ([(20637, 8440, 1347, 4005, 268100, 43968454, "retry"),
                   (537, None, None, None, None, None, "classical_shortcut")], [179, 181]),
     (46927, 0): ([(29890, 12551, 11799, 23240, 184809, 175938419, "retry"),
@@ -107,7 +109,7 @@ def _reference_amplitude(q: int, M: int) -> complex:
     return complex((a / np.sqrt(w.sum()))[0])
 
 
-@pytest.mark.parametrize("n,seed", [(32399, 8), (32399, 2), (32399, 0), (46927, 0)])
+@pytest.mark.parametrize("n,seed", [(32399, 8), (32399, 2), (32399, 3), (32399, 0), (46927, 0)])
 def test_run_shor_baseline_config(n, seed, monkeypatch):
     want_attempts, want_factors = TRACES[(n, seed)]
     quantum = [a for a in want_attempts if a[1] is not None]
