@@ -138,3 +138,29 @@ def test_run_shor_baseline_config(n, seed, monkeypatch):
             assert got.candidate.p % r == 0
             assert got.q == 1 << (n * n - 1).bit_length()
     print(f"n={n} seed={seed}:", seen)
+
+
+def test_fixed_base_large_support_q2_30():
+    """SURVEY 8(d)'s fixed-base microbenchmark comb for n = 32399: x = 7 has
+    order r = 1068, so the class of k = 1 collapses to M ~ 1.0e6 amplitudes
+    (31 super-blocks per tile at KCH = 8) -- the int8 engine's longest Horner
+    accumulation over super-blocks among the documented cases -- checked
+    with the same rows and bars as the driver-run configs."""
+    from types import SimpleNamespace
+
+    from paper_1801_01434_b200 import device as dev
+    from paper_1801_01434_b200 import numtheory as nt
+
+    n, x, q = 32399, 7, 1 << 30
+    r = nt.classical_period(x, n)
+    assert r == 1068
+    c0 = 0  # x^0 = 1: the class of k = 1 starts at a = 0
+    M = (q - 1 - c0) // r + 1
+    amp = complex(_reference_amplitude(q, M))
+    out, prob, bsum = dev.dft_uniform(amp, M, c0, r, q, 0, q)
+    spec = dev.DeviceSpectrum(q, out, prob, bsum)
+    state = SimpleNamespace(q=q, full_comb=True, a0=c0, stride=r, length=M, amp=amp)
+    report = {"M": M}
+    _check_spectrum(state, spec, 0, report)
+    assert abs(dev.dsum(bsum) - 1.0) < 1e-9, report
+    print("fixed base x=7:", report)
