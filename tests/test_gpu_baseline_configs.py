@@ -164,3 +164,35 @@ def test_fixed_base_large_support_q2_30():
     _check_spectrum(state, spec, 0, report)
     assert abs(dev.dsum(bsum) - 1.0) < 1e-9, report
     print("fixed base x=7:", report)
+
+
+@pytest.mark.parametrize("engine", ["fp32", "mma"])
+def test_other_engines_at_the_north_star_comb(engine, monkeypatch):
+    """The north star's seed-2 comb (n = 32399, q = 2^30, M = 201075) on the
+    FP32 fast path (tcgen05, bar max|dp| <= 1e-4 max p) and on the FP64 DMMA
+    engine (SHB_DFT_ENGINE=mma, the same FP64 bars as the default engine) --
+    10^6 random rows plus every peak row against the closed form."""
+    from paper_1801_01434_b200 import device as dev
+
+    q, c0, r, M = 1 << 30, 4828, 5340, 201075
+    amp = complex(_reference_amplitude(q, M))
+    if engine == "mma":
+        monkeypatch.setenv("SHB_DFT_ENGINE", "mma")
+    out, prob, bsum = dev.dft_uniform(amp, M, c0, r, q, 0, q, precision="fp32" if engine == "fp32" else "fp64")
+    rng = np.random.default_rng(11)
+    j = np.arange(r, dtype=np.uint64)
+    peaks = (2 * j * np.uint64(q) + np.uint64(r)) // np.uint64(2 * r) % np.uint64(q)
+    rows = np.unique(np.concatenate([peaks, rng.integers(0, q, 1_000_000, dtype=np.uint64)]))
+    t = torch.from_numpy(rows.astype(np.int64)).cuda()
+    got_p = prob[t].cpu().numpy()
+    pcf = oracle.comb_probabilities_vec(q, r, c0, M, rows)
+    dp = float(np.abs(got_p - pcf).max()) / float(pcf.max())
+    if engine == "fp32":
+        assert dp <= 1e-4, dp
+    else:
+        got = out.view(torch.complex128)[t].cpu().numpy()
+        exact = oracle.comb_rows_exact(q, r, c0, M, amp, rows)
+        dv = float(np.abs(got - exact).max()) / float(np.abs(exact).max())
+        assert dv <= V_TOL and dp <= P_TOL, (dv, dp)
+    assert abs(dev.dsum(bsum) - 1.0) < (1e-5 if engine == "fp32" else 1e-9)
+    print(engine, "max|dp|/max p", dp)
